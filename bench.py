@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Benchmark of the PSFS hot path (BASELINE.json metric: voxel-camera
+projections/s and frames/s, 128^3 grid, 8 cameras 640x480, on 1/2/4/8 B200).
+
+A step = one pass of the whole hot path (stage 1 likelihood terms + stage 2
+projection / fusion / threshold / bit packing) over one batch of B distinct
+synthetic frame sets (config C2, BASELINE.json configs[1]).  Multi-GPU is
+frame-parallel (weak scaling): every rank reconstructs its own batch, no
+collective on the data path; time = max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+Prints one JSON line on rank 0.  `--impl reference` times the CPU oracle (this
+tier's reference arm) on the host cores on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "voxel-camera projections/s and frames/s (128^3, 8 cams) at 1/2/4/8 B200"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=8, help="frames per step per GPU")
+    ap.add_argument("--pool", type=int, default=16, help="distinct frame sets cycled")
+    ap.add_argument("--fuse", type=int, default=8, help="frames fused per kernel pass")
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--profile", action="store_true",
+                    help="ncu mode: no clocks sampling / cpu baseline / e2e")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        time.sleep(0.05)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- helpers
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def make_workload(config, n_distinct, seed_offset=0):
+    from synth.scene import make_frames, make_scene
+    s = make_scene(config)
+    frames = np.stack([make_frames(s, seed_offset + f) for f in range(n_distinct)])
+    return s, frames
+
+
+def cpu_baseline(scene, frames, seconds, nthreads):
+    """The oracle as it stands, on the host cores, over whole frames until
+    `seconds` of work (at least one frame)."""
+    import oracle
+    oracle.build()
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        oracle.scene_reconstruct(scene, frames[n % len(frames)], nthreads=nthreads)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return n / el, n, el
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    rank, world, local = dist_setup(args)
+    if rank != 0:
+        return  # rank 0 alone runs and prints the CPU oracle arm
+    from synth.scene import CONFIGS
+    scene, frames = make_workload(args.config, min(args.pool, 4))
+    nthreads = host_cores()
+    import oracle
+    oracle.build()
+    for w in range(max(args.warmup, 0)):
+        oracle.scene_reconstruct(scene, frames[w % len(frames)], nthreads=nthreads)
+    times = []
+    for k in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.scene_reconstruct(scene, frames[k % len(frames)], nthreads=nthreads)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    fps = args.steps / total
+    nvc = scene.grid.nvox * scene.ncam
+    out = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+        "voxel_camera_projections_per_s": fps * nvc,
+        "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}",
+                   "frames_per_step": 1, "grid": [scene.grid.xlen] * 3, "cameras": scene.ncam},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": nthreads, "kind": "oracle",
+                         "sample": f"1 full {args.config} frame per step (plain C oracle, "
+                                   f"OpenMP over z-slices, {nthreads} threads)"},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1311_6811_b200 import build as pbuild
+    if rank == 0:
+        pbuild.build()
+    if world > 1:
+        dist.barrier()
+    from paper_1311_6811_b200 import from_scene
+    from synth.scene import CONFIGS
+
+    B = args.batch
+    pool = max(args.pool, B)
+    # every rank reconstructs different frames (frame-parallel, weak scaling)
+    scene, frames = make_workload(args.config, pool, seed_offset=rank * pool)
+    rec = from_scene(scene, device=local)
+    rec.set_max_fuse(args.fuse)
+    frames_dev = torch.from_numpy(frames).to(dev)
+    L, Bits = rec.alloc_outputs(B, logodds=False, bits=True)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    nvox, ncam = scene.grid.nvox, scene.ncam
+    per_cam = frames[0, 0].nbytes
+
+    def step(k):
+        i0 = (k * B) % pool
+        idx = [(i0 + b) % pool for b in range(B)]
+        if idx == list(range(idx[0], idx[0] + B)):
+            fr = frames_dev[idx[0]: idx[0] + B]
+        else:
+            fr = frames_dev[idx]
+        rec.reconstruct_batch(fr, B, logodds=None, bits=Bits, stream=stream)
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize(dev)
+
+    # ---- timed region: K steps, L2 flushed between steps (outside the events)
+    sampler = ClockSampler(local) if not args.profile else None
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    rec.set_profiling(True)
+    rec.kernel_times(reset=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    launches = 0
+    for k in range(args.steps):
+        flush.fill_(k)
+        ev[k][0].record(stream)
+        step(args.warmup + k)
+        ev[k][1].record(stream)
+        launches += rec.last_launch_count
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    kt = rec.kernel_times(reset=True)
+    rec.set_profiling(False)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    frames_total = world * B * args.steps
+    fps = frames_total / (total_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (per-launch averages inside the timed region)
+    import json as _json
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = _json.load(f)
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"
+    roi = rec.roi()
+    roi_px = int(((roi[:, 1] - roi[:, 0]).astype(np.int64) * (roi[:, 3] - roi[:, 2])).sum())
+    F = args.fuse
+    groups_per_step = B // F
+    l_ms, l_n = kt["k_likelihood"]
+    v_ms, v_n = kt["k_voxel"]
+    # stage 1 algorithmic bytes per launch (F frames fused): model 24 B/px once,
+    # image 3 B/px and term 4 B/px per frame, over the planned pixel rectangle
+    s1_bytes = roi_px * (24 + 7 * F)
+    s1_avg_s = (l_ms / max(l_n, 1)) / 1e3
+    s1_gbs = s1_bytes / s1_avg_s / 1e9 if s1_avg_s > 0 else 0.0
+    # stage 2: voxel-camera projections per launch
+    vc_per_launch = nvox * ncam * F
+    v_avg_s = (v_ms / max(v_n, 1)) / 1e3
+    dominant = "k_likelihood" if l_ms >= v_ms else "k_voxel"
+    kernel_share = {"k_likelihood": l_ms / max(l_ms + v_ms, 1e-12),
+                    "k_voxel": v_ms / max(l_ms + v_ms, 1e-12)}
+    roofline = {"kernel": "k_likelihood", "bound": "hbm", "achieved": s1_gbs, "peak": hbm_peak,
+                "unit": "GB/s", "frac": s1_gbs / hbm_peak, "traffic": None,
+                "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": s1_bytes, "avg_launch_us": s1_avg_s * 1e6,
+                "dominant_kernel": dominant, "kernel_share": kernel_share,
+                "k_voxel": {"avg_launch_us": v_avg_s * 1e6,
+                            "voxel_cam_frames_per_s": vc_per_launch / v_avg_s if v_avg_s else 0}}
+
+    # ---- end to end through the C ABI with HOST buffers (pinned), per step:
+    # H2D of the batch's frames, both stages, D2H of the bitmask
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        hframes = torch.from_numpy(frames).pin_memory()
+        hbits = torch.zeros((B, scene.grid.nwords), dtype=torch.int32).pin_memory()
+        hb = [hframes[(k * B) % (pool - B + 1):(k * B) % (pool - B + 1) + B] for k in range(4)]
+        for k in range(3):
+            rec.reconstruct_host(hb[k % 4], B, None, hbits, stream=stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(args.steps):
+            rec.reconstruct_host(hb[k % 4], B, None, hbits, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e_ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": world * B * args.steps / (e_ms / 1e3), "unit": "frames/s",
+               "h2d_bytes_per_step": int(B * ncam * per_cam),
+               "d2h_bytes_per_step": int(B * scene.grid.nwords * 4),
+               "ms_per_step": e_ms / args.steps,
+               "how": "psfs_reconstruct_host: pinned host frames -> device staging (copy stream), "
+                      "both stages, bitmask -> pinned host (second copy stream), double-buffered"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        nthreads = host_cores()
+        v, n, el = cpu_baseline(scene, frames, args.cpu_seconds, nthreads)
+        cpu = {"value": v, "unit": "frames/s", "cores": nthreads, "kind": "oracle",
+               "sample": f"{n} full {args.config} frames ({el:.1f} s of work), plain C oracle "
+                         f"(double; OpenMP over z-slices)"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64+f32+i32", "data": "synthetic",
+            "voxel_camera_projections_per_s": fps * nvox * ncam,
+            "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}",
+                       "frames_per_step_per_gpu": B, "fused_frames_per_pass": F,
+                       "grid": [scene.grid.xlen, scene.grid.ylen, scene.grid.zlen],
+                       "cameras": ncam, "image": [int(scene.widths[0]), int(scene.heights[0])],
+                       "distinct_frame_sets": pool, "parallelism": f"frame-parallel x{world}",
+                       "l2": "flushed between steps (256 MiB fill, outside the step events)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clocks,
+            "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms),
+                        "max": max(step_ms)},
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

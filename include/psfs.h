@@ -1,0 +1,200 @@
+/*
+ * psfs.h -- C ABI of the B200-native probabilistic shape-from-silhouette (PSFS)
+ * hot path of arXiv 1311.6811 ("Digitize Your Body and Action in 3-D at Over
+ * 10 FPS"), section 2.2.2.
+ *
+ * Citation keys: P:n = PAPER.md line n; S:n = SPEC.md line n; R#n = reading n
+ * in DESIGN.md ("Readings of the paper").
+ *
+ * What the library computes ("given a set of images ... calculate the
+ * silhouette likelihood maps ... estimate the posterior probability
+ * representing occupancy of each voxel"):
+ *
+ *   stage 1, per pixel p of camera r (Eq 1-2, and Eq 5-9):
+ *     d   = sum_ch ln N(I_ch | mu_ch, sigma'_ch) - ln U,  U = 256^-3   (R#2-R#4)
+ *     SLM = 1 / (1 + e^d)
+ *     t   = ln P(S|V=1) - ln P(S|V=0)
+ *         = ln SLM - ln((1-p_O)(1-SLM) + p_O SLM)
+ *         = -logaddexp(ln p_O, ln(1-p_O) + d)
+ *     stored as the fixed-point integer q = rint(t * 2^20)            (R#16)
+ *   stage 2, per voxel (i,j,k) (Eq 3-4; threshold P:111):
+ *     for each camera, project the voxel centre to its nearest pixel (
+ *     pinned FP32 arithmetic, R#10-R#13); out-of-view views contribute t = 0
+ *     (SLM = 1/2, R#12);  S = sum of the in-view q;
+ *     log-odds L = S * 2^-20 + logit(p_V);   occupied <=> L > logit(tau)
+ *     (<=> posterior > tau, R#14), bit v = i + xlen (j + ylen k) of a uint32
+ *     word array, word v >> 5, bit v & 31, LSB first (R#19).
+ *
+ * Conventions for every call:
+ *   - Return value: PSFS_OK (0) or a positive PSFS_E* code.  No exception or
+ *     abort ever crosses the ABI.  psfs_last_error(h) gives detail text.
+ *   - Ownership: the caller owns every buffer it passes.  psfs_set_* copy their
+ *     HOST inputs into library-owned device memory and return after the copy.
+ *   - psfs_reconstruct* are asynchronous on the given CUDA stream (a
+ *     cudaStream_t passed as void*, NULL = the legacy default stream): inputs
+ *     must stay valid and outputs must not be read until the stream reaches
+ *     that point.  Calls that enqueue work on the same handle must use one
+ *     stream at a time (the handle owns one term buffer).
+ *   - A handle is bound to one CUDA device and is not thread-safe.
+ */
+#ifndef PSFS_H
+#define PSFS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    PSFS_OK = 0,
+    PSFS_EINVAL = 1,      /* NULL where required; both outputs NULL; non-finite or
+                             out-of-range values (priors or tau not in (0,1), spacing
+                             <= 0, sizes <= 0); fixed-point headroom exceeded
+                             (ncam * max|t| * 2^20 >= 2^31); unaligned pointers   */
+    PSFS_EDEGENERATE = 2, /* camera 3x3 block singular, or W/H <= 0      */
+    PSFS_EDIM = 3,        /* background size != camera size                */
+    PSFS_ECOUNT = 4,      /* some camera has no background model yet      */
+    PSFS_ESTATE = 5,      /* call order violated (cameras before backgrounds ...)  */
+    PSFS_ECUDA = 6,       /* a CUDA runtime call or kernel launch failed           */
+    PSFS_ENOMEM = 7,      /* device allocation failed                              */
+    PSFS_ELIMIT = 8       /* more cameras / frames than this build supports        */
+};
+
+#define PSFS_MAX_CAMERAS 64 /* per handle                                  */
+#define PSFS_MAX_BATCH 8    /* frames fused into one stage-1/stage-2 pass  */
+
+typedef struct psfs_handle psfs_handle; /* opaque, library-owned */
+
+/* Volume of interest ("xlen ... ylen ... zlen").
+ * Voxel (i,j,k) centre = origin + spacing * (idx + 1/2) in mm (R#13). */
+typedef struct {
+    double origin[3];
+    double spacing;
+    int32_t xlen, ylen, zlen;
+} psfs_grid;
+
+/* Model constants.  psfs_default_params() fills the defaults below. */
+typedef struct {
+    double occlusion_prior; /* P(O=1), Eq 5: 0.5; in (0,1)           (R#7)  */
+    double voxel_prior;     /* P(V=1), Eq 3: 0.5; in (0,1)                 (R#8)  */
+    double threshold;       /* tau: occupied iff posterior > tau, 0.5      (R#14) */
+    double sigma_floor;     /* sigma' = max(sigma, floor), 1.0 grey level  (R#6)  */
+} psfs_params;
+
+/* Placement of this handle in a z-slab partition of the grid (DESIGN.md
+ * "Multi-GPU").  world = 1: the handle computes the whole grid.  world > 1:
+ * the handle computes slices [k0, k1) with k0 = rank*zlen/world; requires
+ * zlen % world == 0 and xlen*ylen*(zlen/world) % 32 == 0 so every slab is a
+ * whole number of bitmask words.  The bitmask exchange (all-gather) between
+ * ranks is the caller's (NCCL through torch.distributed in the Python layer). */
+typedef struct {
+    int32_t device; /* CUDA device ordinal the handle allocates on            */
+    int32_t rank;   /* 0 <= rank < world                                       */
+    int32_t world;  /* >= 1                                                    */
+} psfs_dist;
+
+void psfs_default_params(psfs_params *out);
+
+/* Create a handle.  dist may be NULL (device = current device, world = 1).
+ * Errors: PSFS_EINVAL (NULL grid/out, bad sizes or params, slab not
+ * word-aligned), PSFS_ECUDA. */
+int psfs_create(const psfs_grid *grid, const psfs_params *params, const psfs_dist *dist,
+                psfs_handle **out);
+
+/* Set the calibrated cameras.  P: HOST, ncam*12 doubles, camera c's
+ * row-major 3x4 matrix mapping homogeneous world mm to homogeneous pixels with
+ * pixel centres at integer coordinates; width/height: HOST, ncam each.  The
+ * library pre-composes A_c = S P_c T in double and rounds it once to float
+ * (DESIGN.md "Pinned projection").  Resets every background model.
+ * Errors: PSFS_EINVAL, PSFS_ELIMIT (ncam > PSFS_MAX_CAMERAS), PSFS_EDEGENERATE,
+ * PSFS_ENOMEM, PSFS_ECUDA. */
+int psfs_set_cameras(psfs_handle *h, int32_t ncam, const double *P, const int32_t *width,
+                     const int32_t *height);
+
+/* Set camera `cam`'s single-Gaussian background model: mean and sigma
+ * (a standard deviation per channel, R#2), HOST, height*width*3 floats each,
+ * row-major, channel-interleaved (the frame layout).  sigma is clamped to
+ * sigma_floor (R#6).  Errors: PSFS_ESTATE (no cameras), PSFS_EINVAL (cam out
+ * of range, NULL, non-finite values), PSFS_EDIM (width/height differ from the
+ * camera's), PSFS_ECUDA. */
+int psfs_set_background(psfs_handle *h, int32_t cam, int32_t width, int32_t height,
+                        const float *mean, const float *sigma);
+
+/* Reconstruct one frame set.  frames: HOST array of ncam DEVICE pointers, each
+ * an H_c*W_c*3 uint8 RGB image (row-major, channel-interleaved), 4-byte aligned.
+ * logodds: DEVICE, nullable, float per voxel of this handle's slab
+ * (xlen*ylen*(k1-k0), x-fastest, slab-relative).  bits: DEVICE, nullable,
+ * ceil(xlen*ylen*zlen/32) uint32 words for the FULL grid; this handle writes
+ * the words of its own slab only.  At least one output must be non-NULL.
+ * Errors: PSFS_EINVAL, PSFS_ESTATE, PSFS_ECOUNT, PSFS_ECUDA. */
+int psfs_reconstruct(psfs_handle *h, const uint8_t *const *frames, float *logodds, uint32_t *bits,
+                     void *cuda_stream);
+
+/* Reconstruct nframes frame sets in one call (frame-batched: the background
+ * model is read once per group of up to PSFS_MAX_BATCH frames and every voxel
+ * projection is computed once per group).  frames: HOST array of nframes*ncam
+ * DEVICE pointers, frame-major (frames[f*ncam + c]).  logodds: nullable,
+ * nframes consecutive slab arrays; bits: nullable, nframes consecutive
+ * full-grid word arrays.  Same errors as psfs_reconstruct. */
+int psfs_reconstruct_batch(psfs_handle *h, int32_t nframes, const uint8_t *const *frames,
+                           float *logodds, uint32_t *bits, void *cuda_stream);
+
+/* End-to-end variant with HOST buffers (the paper's non-blocking transfers on
+ * several command queues): frames: HOST array of nframes*ncam HOST
+ * pointers (page-locked memory gives real overlap), frame-major; logodds /
+ * bits: nullable HOST outputs laid out as in psfs_reconstruct_batch.  The
+ * library copies each group of frames into its own device staging buffers on
+ * an internal copy stream, computes on cuda_stream, and copies the results back
+ * on a second copy stream, double-buffered so group g+1's upload and group
+ * g-1's download overlap group g's kernels.  Asynchronous: host outputs are
+ * valid once cuda_stream has reached the end of the call (synchronize it).
+ * Same errors as psfs_reconstruct_batch, plus PSFS_ENOMEM for the staging. */
+int psfs_reconstruct_host(psfs_handle *h, int32_t nframes, const uint8_t *const *frames,
+                          float *logodds, uint32_t *bits, void *cuda_stream);
+
+void psfs_destroy(psfs_handle *h);
+
+const char *psfs_status_string(int status);
+const char *psfs_last_error(const psfs_handle *h);
+
+/* ---- introspection (tests, planner) ------------------------------------ */
+
+/* This handle's slab [k0, k1). */
+int psfs_slab(const psfs_handle *h, int32_t *k0, int32_t *k1);
+
+/* The pre-composed float matrices A_c (HOST out, ncam*12). */
+int psfs_debug_matrices(const psfs_handle *h, float *out);
+
+/* Stage 1 only, for one frame set over whole images: writes q (int32 Q11.20)
+ * for every pixel, cameras concatenated in order (DEVICE out, sum_c W_c*H_c).
+ * Asynchronous on cuda_stream. */
+int psfs_debug_terms(psfs_handle *h, const uint8_t *const *frames, int32_t *terms_out,
+                     void *cuda_stream);
+
+/* Per-camera stage-1 region of interest the planner computed for this
+ * handle's slab: HOST out, ncam*4 int32 (row0, row1, col0, col1), half-open;
+ * every pixel a voxel of the slab can project to lies inside it. */
+int psfs_debug_roi(const psfs_handle *h, int32_t *out);
+
+/* Enable/disable the ROI restriction of stage 1 (default on). */
+int psfs_set_roi_enabled(psfs_handle *h, int32_t enabled);
+
+/* Cap the number of frames fused into one pass (1, 2, 4 or 8; default 8). */
+int psfs_set_max_fuse(psfs_handle *h, int32_t fmax);
+
+/* Per-kernel device timing (bench instrumentation): when enabled, every
+ * stage-1 and stage-2 launch is bracketed by CUDA events on the launching
+ * stream.  psfs_kernel_times synchronizes those events and returns the summed
+ * milliseconds and launch counts of [0] k_likelihood and [1] k_voxel since the
+ * last reset (HOST outs, 2 entries each; either may be NULL). */
+int psfs_set_profiling(psfs_handle *h, int32_t enabled);
+int psfs_kernel_times(psfs_handle *h, double *ms, int64_t *launches, int32_t reset);
+
+/* Number of kernel launches the last psfs_reconstruct* call enqueued. */
+int psfs_last_launch_count(const psfs_handle *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSFS_H */

@@ -1,0 +1,57 @@
+// psfs_internal.h -- shared between the host runtime (psfs_api.cu) and the
+// sm_100a kernels (psfs_kernels.cu).  Not part of the public ABI (include/psfs.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace psfs {
+
+constexpr int kMaxCam = 64;  // == PSFS_MAX_CAMERAS
+constexpr int kMaxF = 8;     // == PSFS_MAX_BATCH
+constexpr int kQBits = 20;   // Q11.20 fixed point for the per-view term t
+
+// Stage 1 (per-pixel term) launch description.
+struct S1Cam {
+    int32_t W, H;
+    int32_t r0, r1, c0, c1;  // region of interest, half-open; c0, c1 multiples of 4 (VEC path)
+    int64_t off;             // first pixel of this camera in the concatenated pixel space
+};
+
+struct S1Params {
+    S1Cam cam[kMaxCam];
+    const uint8_t *frames[kMaxF][kMaxCam];  // [f][c] device pointers, H*W*3 RGB
+    const float *mu;                        // 3 planes of total_px floats
+    const float *sg;                        // 3 planes of total_px floats (sigma', floored)
+    int32_t *terms;                         // (off + p) * F + f
+    int64_t total_px;
+    double ln_po;    // ln p_O
+    double ln_1mpo;  // ln (1 - p_O)
+    double c0;       // -1.5 ln(2 pi) - ln U = 24 ln 2 - 1.5 ln(2 pi)
+    int32_t ncam;
+};
+
+// Stage 2 (voxel) launch description.
+struct VCam {
+    float A[12];   // pre-composed pinned projection matrix, row-major 3x4
+    int32_t W, H;
+    int64_t off;   // pixel offset of this camera's term image
+};
+
+struct VParams {
+    VCam cam[kMaxCam];
+    const int32_t *terms;
+    uint32_t *bits[kMaxF];   // full-grid word arrays (nullable)
+    float *logodds[kMaxF];   // slab arrays (nullable)
+    int32_t xlen, ylen, k0, k1;
+    int32_t ncam;
+    int32_t Tq;              // occupied iff S > Tq
+    int32_t aligned;         // xlen % 32 == 0: one whole word per warp row
+    double logit_pv;
+};
+
+// Launchers (psfs_kernels.cu).  Return the cudaError_t of the launch.
+cudaError_t launch_likelihood(const S1Params &p, int F, bool vec4, int max_rows_px,
+                              cudaStream_t s);
+cudaError_t launch_voxel(const VParams &p, int F, bool want_logodds, cudaStream_t s);
+
+}  // namespace psfs

@@ -1,0 +1,98 @@
+"""Multi-GPU partition of the PSFS path.
+
+One process per GPU (torchrun), torch.distributed for the plumbing:
+
+* frame-parallel ("weak" scaling, configs C2/C3/C5 sequences): rank r takes
+  frames r, r+N, ...; each rank is an independent single-GPU handle, no
+  collective on the data path (voxels and frames are independent, PAPER.md:228
+  "the procedures for each voxel has nothing to do with others", and the
+  uniform foreground model makes frames independent, R#17).
+* z-slab (config C4): rank r owns slices [r*zlen/N, (r+1)*zlen/N) of the grid
+  (the library's psfs_dist), runs stage 1 only on the pixel rectangle its slab
+  projects into, stage 2 on its slab, and the full occupancy bitmask is
+  assembled on every rank by one in-place all-gather of the per-slab words
+  (NCCL over NVLink on GPUs; gloo in the CPU tests).  Log-odds stay sharded.
+
+The slab rule here is the same pure function the library applies
+(k0 = zlen*rank//world); tests check both agree.
+"""
+from __future__ import annotations
+
+import os
+
+
+def slab_bounds(zlen: int, world: int, rank: int):
+    """[k0, k1) of rank's z-slab (integer rule of psfs_create)."""
+    return zlen * rank // world, zlen * (rank + 1) // world
+
+
+def check_partition(xlen: int, ylen: int, zlen: int, world: int):
+    """z-slab mode needs equal slabs of whole bitmask words."""
+    if zlen % world:
+        raise ValueError(f"zlen={zlen} not divisible by world={world}")
+    if (xlen * ylen * (zlen // world)) % 32:
+        raise ValueError("slab is not a whole number of 32-bit words")
+
+
+def slab_words(xlen, ylen, zlen, world, rank):
+    k0, k1 = slab_bounds(zlen, world, rank)
+    return xlen * ylen * k0 // 32, xlen * ylen * k1 // 32
+
+
+def frame_indices(nframes: int, world: int, rank: int):
+    """Frame-parallel assignment: rank r takes r, r+N, r+2N, ..."""
+    return list(range(rank, nframes, world))
+
+
+def allgather_bits(bits, xlen, ylen, zlen, world, rank, group=None):
+    """In-place all-gather of slab words: bits is an int32 tensor [nframes, nwords]
+    (or [nwords]) holding this rank's slab words; afterwards every rank holds the
+    full grid.  One collective per frame row (all_gather_into_tensor)."""
+    import torch
+    import torch.distributed as dist
+    check_partition(xlen, ylen, zlen, world)
+    if world == 1:
+        return bits
+    b = bits if bits.dim() == 2 else bits.unsqueeze(0)
+    nwords = xlen * ylen * zlen // 32
+    chunk = nwords // world
+    for f in range(b.shape[0]):
+        row = b[f, :nwords]
+        mine = row[rank * chunk:(rank + 1) * chunk]
+        if row.is_cuda:
+            dist.all_gather_into_tensor(row, mine, group=group)
+        else:  # gloo has no in-place all_gather_into_tensor: gather a list
+            parts = [torch.empty_like(mine) for _ in range(world)]
+            dist.all_gather(parts, mine.clone(), group=group)
+            row.copy_(torch.cat(parts))
+    return bits
+
+
+def env_rank_world():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class ZSlabReconstructor:
+    """A z-slab handle plus the bitmask all-gather (NCCL process group)."""
+
+    def __init__(self, scene, params=None, rank=None, world=None, device=None, group=None):
+        from .psfs import from_scene
+        r, w, local = env_rank_world()
+        self.rank = r if rank is None else rank
+        self.world = w if world is None else world
+        g = scene.grid
+        check_partition(g.xlen, g.ylen, g.zlen, self.world)
+        self.grid = g
+        self.group = group
+        self.rec = from_scene(scene, params, device=local if device is None else device,
+                              rank=self.rank, world=self.world)
+
+    def reconstruct_batch(self, frames, nframes, logodds=None, bits=None, stream=None,
+                          gather=True):
+        self.rec.reconstruct_batch(frames, nframes, logodds=logodds, bits=bits, stream=stream)
+        if gather and bits is not None:
+            g = self.grid
+            allgather_bits(bits, g.xlen, g.ylen, g.zlen, self.world, self.rank, self.group)

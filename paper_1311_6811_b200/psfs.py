@@ -1,0 +1,339 @@
+"""Thin ctypes binding of the C ABI in include/psfs.h (argument marshalling only).
+
+Every step of the PSFS path runs in the sm_100a kernels of libpsfs.so; this
+module converts torch tensors / numpy arrays into the pointers and sizes the
+ABI takes.  There is no CPU fallback: if libpsfs.so is missing or the device
+is not a CUDA GPU, every call raises.
+
+PyTorch supplies device memory (torch.empty(..., device='cuda')), streams
+(torch.cuda.current_stream().cuda_stream) and, in parallel.py, process groups.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpsfs.so")
+
+PSFS_OK = 0
+STATUS = {0: "PSFS_OK", 1: "PSFS_EINVAL", 2: "PSFS_EDEGENERATE", 3: "PSFS_EDIM", 4: "PSFS_ECOUNT",
+          5: "PSFS_ESTATE", 6: "PSFS_ECUDA", 7: "PSFS_ENOMEM", 8: "PSFS_ELIMIT"}
+MAX_CAMERAS = 64
+MAX_BATCH = 8
+
+# Every symbol include/psfs.h declares (checked by tests/test_abi.py).
+EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_background",
+           "psfs_reconstruct", "psfs_reconstruct_batch", "psfs_reconstruct_host", "psfs_destroy",
+           "psfs_status_string", "psfs_last_error", "psfs_slab", "psfs_debug_matrices",
+           "psfs_debug_terms", "psfs_debug_roi", "psfs_set_roi_enabled", "psfs_set_max_fuse",
+           "psfs_last_launch_count", "psfs_set_profiling", "psfs_kernel_times"]
+
+
+class PsfsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Grid(C.Structure):
+    _fields_ = [("origin", C.c_double * 3), ("spacing", C.c_double),
+                ("xlen", C.c_int32), ("ylen", C.c_int32), ("zlen", C.c_int32)]
+
+
+class Params(C.Structure):
+    _fields_ = [("occlusion_prior", C.c_double), ("voxel_prior", C.c_double),
+                ("threshold", C.c_double), ("sigma_floor", C.c_double)]
+
+
+class Dist(C.Structure):
+    _fields_ = [("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libpsfs.so (built by __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, d = C.c_void_p, C.c_int32, C.c_double
+        L.psfs_default_params.argtypes = [C.POINTER(Params)]
+        L.psfs_default_params.restype = None
+        L.psfs_create.argtypes = [C.POINTER(Grid), C.POINTER(Params), C.POINTER(Dist), C.POINTER(vp)]
+        L.psfs_set_cameras.argtypes = [vp, i32, vp, vp, vp]
+        L.psfs_set_background.argtypes = [vp, i32, i32, i32, vp, vp]
+        L.psfs_reconstruct.argtypes = [vp, vp, vp, vp, vp]
+        L.psfs_reconstruct_batch.argtypes = [vp, i32, vp, vp, vp, vp]
+        L.psfs_reconstruct_host.argtypes = [vp, i32, vp, vp, vp, vp]
+        L.psfs_destroy.argtypes = [vp]
+        L.psfs_destroy.restype = None
+        L.psfs_status_string.argtypes = [C.c_int]
+        L.psfs_status_string.restype = C.c_char_p
+        L.psfs_last_error.argtypes = [vp]
+        L.psfs_last_error.restype = C.c_char_p
+        L.psfs_slab.argtypes = [vp, C.POINTER(i32), C.POINTER(i32)]
+        L.psfs_debug_matrices.argtypes = [vp, vp]
+        L.psfs_debug_terms.argtypes = [vp, vp, vp, vp]
+        L.psfs_debug_roi.argtypes = [vp, vp]
+        L.psfs_set_roi_enabled.argtypes = [vp, i32]
+        L.psfs_set_max_fuse.argtypes = [vp, i32]
+        L.psfs_last_launch_count.argtypes = [vp]
+        L.psfs_set_profiling.argtypes = [vp, i32]
+        L.psfs_kernel_times.argtypes = [vp, vp, vp, i32]
+        _lib = L
+    return _lib
+
+
+def default_params() -> dict:
+    p = Params()
+    lib().psfs_default_params(C.byref(p))
+    return dict(occlusion_prior=p.occlusion_prior, voxel_prior=p.voxel_prior,
+                threshold=p.threshold, sigma_floor=p.sigma_floor)
+
+
+def _ptr_array(ptrs):
+    arr = (C.c_void_p * len(ptrs))(*[int(p) for p in ptrs])
+    return arr
+
+
+def _dev_ptr(t, dtype=None):
+    import torch
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("expected a CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"expected dtype {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return t.data_ptr()
+
+
+@dataclass
+class GridSpec:
+    origin: tuple
+    spacing: float
+    xlen: int
+    ylen: int
+    zlen: int
+
+    @property
+    def nvox(self):
+        return self.xlen * self.ylen * self.zlen
+
+    @property
+    def nwords(self):
+        return (self.nvox + 31) // 32
+
+
+class Reconstructor:
+    """One library handle (psfs_create ... psfs_destroy) on one CUDA device."""
+
+    def __init__(self, grid, params: dict | None = None, device: int | None = None,
+                 rank: int = 0, world: int = 1):
+        import torch
+        self._h = None
+        g = Grid((C.c_double * 3)(*[float(x) for x in grid.origin]), float(grid.spacing),
+                 int(grid.xlen), int(grid.ylen), int(grid.zlen))
+        p = Params()
+        lib().psfs_default_params(C.byref(p))
+        for k, v in (params or {}).items():
+            setattr(p, k, float(v))
+        if device is None:
+            device = torch.cuda.current_device()
+        dist = Dist(int(device), int(rank), int(world))
+        h = C.c_void_p()
+        rc = lib().psfs_create(C.byref(g), C.byref(p), C.byref(dist), C.byref(h))
+        if rc != PSFS_OK:
+            raise PsfsError(rc, "psfs_create failed")
+        self._h = h
+        self.grid = GridSpec(tuple(grid.origin), float(grid.spacing), int(grid.xlen),
+                             int(grid.ylen), int(grid.zlen))
+        self.device = int(device)
+        self.rank, self.world = int(rank), int(world)
+        k0, k1 = C.c_int32(), C.c_int32()
+        lib().psfs_slab(h, C.byref(k0), C.byref(k1))
+        self.k0, self.k1 = k0.value, k1.value
+        self.ncam = 0
+        self.widths = self.heights = None
+
+    # -- lifecycle ---------------------------------------------------------
+    def close(self):
+        if self._h is not None:
+            lib().psfs_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc, what):
+        if rc != PSFS_OK:
+            msg = lib().psfs_last_error(self._h).decode() if self._h else ""
+            raise PsfsError(rc, f"{what}: {msg}")
+
+    # -- setup -------------------------------------------------------------
+    def set_cameras(self, P, widths, heights):
+        P = np.ascontiguousarray(np.asarray(P, np.float64).reshape(-1, 12))
+        W = np.ascontiguousarray(np.asarray(widths, np.int32))
+        H = np.ascontiguousarray(np.asarray(heights, np.int32))
+        self._check(lib().psfs_set_cameras(self._h, P.shape[0], P.ctypes.data, W.ctypes.data,
+                                           H.ctypes.data), "psfs_set_cameras")
+        self.ncam = P.shape[0]
+        self.widths, self.heights = W.copy(), H.copy()
+        self.npix = int((W.astype(np.int64) * H).sum())
+
+    def set_background(self, cam, mean, sigma):
+        mean = np.ascontiguousarray(np.asarray(mean, np.float32))
+        sigma = np.ascontiguousarray(np.asarray(sigma, np.float32))
+        if mean.ndim != 3 or mean.shape != sigma.shape or mean.shape[2] != 3:
+            raise ValueError("mean/sigma must be [H, W, 3] float32")
+        self._check(lib().psfs_set_background(self._h, int(cam), mean.shape[1], mean.shape[0],
+                                              mean.ctypes.data, sigma.ctypes.data),
+                    "psfs_set_background")
+
+    def set_max_fuse(self, fmax: int):
+        self._check(lib().psfs_set_max_fuse(self._h, int(fmax)), "psfs_set_max_fuse")
+
+    def set_roi_enabled(self, on: bool):
+        self._check(lib().psfs_set_roi_enabled(self._h, int(bool(on))), "psfs_set_roi_enabled")
+
+    # -- outputs -------------------------------------------------------------
+    @property
+    def nslab(self):
+        return self.grid.xlen * self.grid.ylen * (self.k1 - self.k0)
+
+    def alloc_outputs(self, nframes=1, logodds=True, bits=True):
+        import torch
+        dev = torch.device("cuda", self.device)
+        L = torch.empty((nframes, self.nslab), dtype=torch.float32, device=dev) if logodds else None
+        B = torch.zeros((nframes, self.grid.nwords), dtype=torch.int32, device=dev) if bits else None
+        return L, B
+
+    # -- the hot path ---------------------------------------------------------
+    def _frame_ptrs(self, frames, nframes):
+        """frames: a uint8 CUDA tensor [nframes, ncam, H, W, 3] (or [ncam, H, W, 3]
+        when nframes == 1), or a nested list [f][c] of [H, W, 3] tensors."""
+        import torch
+        ptrs = []
+        if isinstance(frames, torch.Tensor):
+            t = frames
+            if t.dim() == 4:
+                t = t.unsqueeze(0)
+            if t.dtype != torch.uint8 or not t.is_cuda or not t.is_contiguous():
+                raise TypeError("frames must be a contiguous uint8 CUDA tensor")
+            if t.shape[0] != nframes or t.shape[1] != self.ncam:
+                raise ValueError("frames shape mismatch")
+            base = t.data_ptr()
+            per_cam = t[0, 0].numel()
+            for f in range(nframes):
+                for c in range(self.ncam):
+                    ptrs.append(base + (f * self.ncam + c) * per_cam)
+        else:
+            for f in range(nframes):
+                row = frames[f] if nframes > 1 or isinstance(frames[0], (list, tuple)) else frames
+                for c in range(self.ncam):
+                    ptrs.append(_dev_ptr(row[c], torch.uint8))
+        return _ptr_array(ptrs)
+
+    def reconstruct_batch(self, frames, nframes: int, logodds=None, bits=None, stream=None):
+        """Enqueue both stages for nframes frame sets on `stream` (default: the
+        current torch stream).  Outputs are caller-owned CUDA tensors:
+        logodds float32 [nframes, nslab], bits int32 [nframes, nwords]."""
+        import torch
+        fp = self._frame_ptrs(frames, nframes)
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        Lp = _dev_ptr(logodds, torch.float32)
+        Bp = _dev_ptr(bits, torch.int32)
+        if logodds is not None and logodds.numel() < nframes * self.nslab:
+            raise ValueError("logodds too small")
+        if bits is not None and bits.numel() < nframes * self.grid.nwords:
+            raise ValueError("bits too small")
+        self._check(lib().psfs_reconstruct_batch(self._h, int(nframes), fp, Lp, Bp, s),
+                    "psfs_reconstruct_batch")
+
+    def reconstruct(self, frames, logodds=None, bits=None, stream=None):
+        import torch
+        fp = self._frame_ptrs(frames, 1)
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._check(lib().psfs_reconstruct(self._h, fp, _dev_ptr(logodds, torch.float32),
+                                           _dev_ptr(bits, torch.int32), s), "psfs_reconstruct")
+
+    def reconstruct_host(self, frames_host, nframes: int, logodds_host=None, bits_host=None,
+                         stream=None):
+        """End-to-end call with HOST buffers (pinned for overlap): the library
+        copies frames in, runs both stages and copies results out, overlapping
+        the transfers of one frame group with the compute of the previous one.
+        frames_host: uint8 tensor/ndarray [nframes, ncam, H, W, 3] in host memory;
+        outputs: host float32 [nframes, nslab] / int32 [nframes, nwords]."""
+        import torch
+        def hp(x):
+            if x is None:
+                return None
+            if isinstance(x, torch.Tensor):
+                assert not x.is_cuda and x.is_contiguous()
+                return x.data_ptr()
+            assert x.flags["C_CONTIGUOUS"]
+            return x.ctypes.data
+        base = hp(frames_host)
+        per_cam = int(self.widths[0]) * int(self.heights[0]) * 3
+        if not (self.widths == self.widths[0]).all() or not (self.heights == self.heights[0]).all():
+            raise ValueError("reconstruct_host helper assumes equal camera sizes")
+        ptrs = _ptr_array([base + i * per_cam for i in range(nframes * self.ncam)])
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._check(lib().psfs_reconstruct_host(self._h, int(nframes), ptrs, hp(logodds_host),
+                                                hp(bits_host), s), "psfs_reconstruct_host")
+
+    # -- introspection ----------------------------------------------------------
+    def debug_terms(self, frames, stream=None):
+        import torch
+        out = torch.empty(self.npix, dtype=torch.int32, device=torch.device("cuda", self.device))
+        fp = self._frame_ptrs(frames, 1)
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._check(lib().psfs_debug_terms(self._h, fp, out.data_ptr(), s), "psfs_debug_terms")
+        return out
+
+    def matrices(self):
+        out = np.empty((self.ncam, 12), np.float32)
+        self._check(lib().psfs_debug_matrices(self._h, out.ctypes.data), "psfs_debug_matrices")
+        return out
+
+    def roi(self):
+        out = np.empty((self.ncam, 4), np.int32)
+        self._check(lib().psfs_debug_roi(self._h, out.ctypes.data), "psfs_debug_roi")
+        return out
+
+    def set_profiling(self, on: bool):
+        self._check(lib().psfs_set_profiling(self._h, int(bool(on))), "psfs_set_profiling")
+
+    def kernel_times(self, reset=True):
+        """{'k_likelihood': (ms, launches), 'k_voxel': (ms, launches)} since last reset."""
+        ms = np.zeros(2, np.float64)
+        n = np.zeros(2, np.int64)
+        self._check(lib().psfs_kernel_times(self._h, ms.ctypes.data, n.ctypes.data, int(reset)),
+                    "psfs_kernel_times")
+        return {"k_likelihood": (float(ms[0]), int(n[0])), "k_voxel": (float(ms[1]), int(n[1]))}
+
+    @property
+    def last_launch_count(self):
+        return int(lib().psfs_last_launch_count(self._h))
+
+
+def from_scene(scene, params=None, device=None, rank=0, world=1) -> Reconstructor:
+    """Build a Reconstructor for a synth.Scene-like object (grid, P, widths,
+    heights, mu, sigma)."""
+    r = Reconstructor(scene.grid, params, device, rank, world)
+    r.set_cameras(scene.P, scene.widths, scene.heights)
+    for c in range(scene.ncam):
+        r.set_background(c, scene.mu[c], scene.sigma[c])
+    return r

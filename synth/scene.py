@@ -314,22 +314,53 @@ def _hit_cylinder(o, d, p0, p1, r):
     return hit, np.where(hit, enter, np.inf)
 
 
+def _part_bbox(cam: Camera, part):
+    """Pixel bounding box (r0, r1, c0, c1) of a part from its axis-aligned
+    bounding box corners; None if some corner is not in front of the camera."""
+    if part[0] == "ellipsoid":
+        lo, hi = part[1] - part[2], part[1] + part[2]
+    else:
+        lo = np.minimum(part[1], part[2]) - part[3]
+        hi = np.maximum(part[1], part[2]) + part[3]
+    corners = np.array([[lo[0] if a else hi[0], lo[1] if b else hi[1], lo[2] if c else hi[2], 1.0]
+                        for a in (0, 1) for b in (0, 1) for c in (0, 1)])
+    x = corners @ cam.P.T
+    if (x[:, 2] <= 1e-6).any():
+        return None
+    u, v = x[:, 0] / x[:, 2], x[:, 1] / x[:, 2]
+    c0 = max(0, int(np.floor(u.min())) - 1)
+    c1 = min(cam.width, int(np.ceil(u.max())) + 2)
+    r0 = max(0, int(np.floor(v.min())) - 1)
+    r1 = min(cam.height, int(np.ceil(v.max())) + 2)
+    return r0, r1, c0, c1
+
+
 def render_labels(cam: Camera, parts) -> np.ndarray:
     """Per-pixel index of the nearest body part hit by the pixel-centre ray
-    (exact ray-quadric / ray-capped-cylinder test); -1 = none."""
-    d = _ray_dirs(cam)
+    (exact ray-quadric / ray-capped-cylinder test); -1 = none.
+    Rays are only cast inside each part's projected bounding box (the part's
+    convex AABB projects inside the hull of its projected corners)."""
+    d_all = _ray_dirs(cam).reshape(cam.height, cam.width, 3)
     o = cam.center
-    best_t = np.full(d.shape[0], np.inf)
-    label = np.full(d.shape[0], -1, np.int16)
+    best_t = np.full((cam.height, cam.width), np.inf)
+    label = np.full((cam.height, cam.width), -1, np.int16)
     for idx, part in enumerate(parts):
+        bb = _part_bbox(cam, part)
+        r0, r1, c0, c1 = bb if bb is not None else (0, cam.height, 0, cam.width)
+        if r1 <= r0 or c1 <= c0:
+            continue
+        d = d_all[r0:r1, c0:c1].reshape(-1, 3)
         if part[0] == "ellipsoid":
             hit, t = _hit_ellipsoid(o, d, part[1], part[2])
         else:
             hit, t = _hit_cylinder(o, d, part[1], part[2], part[3])
-        closer = hit & (t < best_t)
-        best_t = np.where(closer, t, best_t)
-        label = np.where(closer, idx, label)
-    return label.reshape(cam.height, cam.width)
+        hit = hit.reshape(r1 - r0, c1 - c0)
+        t = t.reshape(r1 - r0, c1 - c0)
+        bt = best_t[r0:r1, c0:c1]
+        closer = hit & (t < bt)
+        best_t[r0:r1, c0:c1] = np.where(closer, t, bt)
+        label[r0:r1, c0:c1] = np.where(closer, idx, label[r0:r1, c0:c1])
+    return label
 
 
 def render_silhouette(cam: Camera, parts) -> np.ndarray:

@@ -1,0 +1,272 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded synthetic inputs.  Bar (BASELINE.json north_star): log-odds within
+1e-4 absolute; occupancy bits exact except voxels whose posterior lies within
+1e-4 of tau; stage-1 terms within 1e-6 of the oracle's t = ln P(S|V=1) -
+ln P(S|V=0) (DESIGN.md error budget)."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from synth.scene import Grid, cube_grid, make_frames, make_scene, ring_rig
+from tests.helpers import assert_parity, gpu_run, unpack_bits
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+NTHREADS = max(1, len(os.sched_getaffinity(0)))
+TERM_TOL = 1e-6
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1311_6811_b200 import build
+    build.build()
+
+
+# ------------------------------------------------------------------ stage 1
+
+def _terms_vs_oracle(scene, frames, params=None):
+    from paper_1311_6811_b200 import from_scene
+    params = params or {}
+    rec = from_scene(scene, params)
+    q = rec.debug_terms(torch.from_numpy(frames).cuda()).cpu().numpy().astype(np.float64)
+    t_gpu = q / 2.0 ** 20
+    worst = 0.0
+    off = 0
+    for c in range(scene.ncam):
+        _, l1, l0 = oracle.slm_image(frames[c], scene.mu[c], scene.sigma[c],
+                                     params.get("sigma_floor", 1.0),
+                                     params.get("occlusion_prior", 0.5), NTHREADS)
+        t = (l1 - l0).reshape(-1)
+        n = t.shape[0]
+        worst = max(worst, float(np.abs(t_gpu[off:off + n] - t).max()))
+        off += n
+    return worst
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_stage1_terms(name):
+    s = make_scene(name)
+    fr = make_frames(s, 0)
+    assert _terms_vs_oracle(s, fr) <= TERM_TOL
+
+
+def test_stage1_extreme_pixels():
+    """I = mu at the sigma floor (d = d_max), >= 10 sigma deviations, sigma below
+    the floor, general p_O."""
+    s = make_scene("C1")
+    rng = np.random.default_rng(1)
+    mu = s.mu.copy()
+    sg = s.sigma.copy()
+    fr = make_frames(s, 0)
+    mu[:, ::2, ::2] = np.round(mu[:, ::2, ::2])
+    fr[:, ::2, ::2] = mu[:, ::2, ::2].astype(np.uint8)       # I = mu exactly
+    sg[:, ::4, :] = rng.uniform(0.1, 1.0, size=sg[:, ::4, :].shape)  # below the floor
+    fr[:, 1::4, :] = np.where(mu[:, 1::4, :] < 128, 255, 0)  # far tail
+    s.mu, s.sigma = mu.astype(np.float32), sg.astype(np.float32)
+    for p in (dict(), dict(occlusion_prior=0.3), dict(occlusion_prior=0.9, sigma_floor=2.0)):
+        assert _terms_vs_oracle(s, fr, p) <= TERM_TOL
+
+
+def test_stage1_ragged_width():
+    """W % 4 != 0 takes the scalar (1 pixel/thread) kernel."""
+    s = make_scene("C1", W=66, H=50)
+    fr = make_frames(s, 0)
+    assert _terms_vs_oracle(s, fr) <= TERM_TOL
+
+
+# ------------------------------------------------------------------ end to end
+
+def _parity(scene, frames_list, params=None, fuse=8, roi=True, **kw):
+    params = params or {}
+    g = gpu_run(scene, frames_list, params, fuse=fuse, roi=roi)
+    stats = []
+    for f, fr in enumerate(frames_list):
+        orc = oracle.scene_reconstruct(scene, fr, nthreads=NTHREADS,
+                                       sigma_floor=params.get("sigma_floor", 1.0),
+                                       p_occ=params.get("occlusion_prior", 0.5),
+                                       p_vox=params.get("voxel_prior", 0.5),
+                                       tau=params.get("threshold", 0.5))
+        stats.append(assert_parity(g["L"][f], g["bits"][f], orc, scene.grid.nvox,
+                                   tau=params.get("threshold", 0.5), **kw))
+    return g, stats
+
+
+@pytest.mark.parametrize("name,body", [("C1", "skeleton"), ("C1", "ellipsoid"),
+                                       ("C2", "skeleton"), ("C2", "both")])
+def test_end_to_end_single_frame(name, body):
+    s = make_scene(name, body=body)
+    _, st = _parity(s, [make_frames(s, 0)])
+    assert st[0]["occupied"] > 0
+
+
+def test_c2_bench_configuration_batch_of_8():
+    """The bench's launch configuration: C2, F = 8 distinct frames fused."""
+    s = make_scene("C2")
+    frames = [make_frames(s, f) for f in range(8)]
+    g, st = _parity(s, frames, fuse=8)
+    # and every frame of the fused batch equals the same frame run alone (F = 1):
+    # integer sums make the result independent of grouping
+    g1 = gpu_run(s, frames[:3], fuse=1)
+    assert np.array_equal(g1["bits"], g["bits"][:3])
+    assert np.array_equal(g1["L"], g["L"][:3])
+
+
+def test_batch_grouping_13_frames():
+    """13 = 8 + 4 + 1 frames: every group size path, against the oracle."""
+    s = make_scene("C1")
+    frames = [make_frames(s, f) for f in range(13)]
+    _parity(s, frames)
+
+
+@pytest.mark.parametrize("fuse", [1, 2, 4])
+def test_fuse_widths(fuse):
+    s = make_scene("C1")
+    _parity(s, [make_frames(s, f) for f in range(fuse)], fuse=fuse)
+
+
+def test_c3_sequence_frames():
+    """C3 (256^3, 8 cameras 1280x960): frames of the walking / arm-waving
+    sequence, full grid against the oracle."""
+    s = make_scene("C3")
+    frames = [make_frames(s, f, motion=True) for f in (0, 45)]
+    _parity(s, frames)
+
+
+def test_ragged_grid_and_images():
+    """xlen % 32 != 0 (atomic bit path), ylen % 8 != 0, zlen % KZ != 0, W % 4 != 0."""
+    g = Grid((-1000.0, -1000.0, 0.0), 2000.0 / 37, 37, 29, 23)
+    s = make_scene("C1", grid=g, W=66, H=50)
+    _parity(s, [make_frames(s, f) for f in range(3)])
+
+
+def test_general_priors_and_threshold():
+    s = make_scene("C1")
+    p = dict(occlusion_prior=0.3, voxel_prior=0.2, threshold=0.7, sigma_floor=1.5)
+    _parity(s, [make_frames(s, 0), make_frames(s, 1)], params=p)
+
+
+def test_all_background_gives_empty_hull():
+    s = make_scene("C2")
+    g = gpu_run(s, [make_frames(s, 0, mode="background")])
+    assert g["bits"].sum() == 0
+
+
+def test_unseen_voxels_keep_prior():
+    """Grid extending far outside every view: those voxels' log-odds equal
+    logit(p_V) (rounded to float) and they are unoccupied at tau = 1/2."""
+    g = Grid((-6000.0, -6000.0, -3000.0), 12000.0 / 32, 32, 32, 32)
+    s = make_scene("C1", grid=g)
+    for pv in (0.5, 0.35):
+        out = gpu_run(s, [make_frames(s, 0)], params=dict(voxel_prior=pv))
+        orc = oracle.scene_reconstruct(s, make_frames(s, 0), p_vox=pv)
+        unseen = orc["L"] == math.log(pv) - math.log1p(-pv)
+        assert unseen.sum() > 1000
+        assert (out["L"][0][unseen] == np.float32(math.log(pv) - math.log1p(-pv))).all()
+
+
+def test_camera_permutation_bit_identical():
+    """Fixed-point accumulation: permuting the cameras leaves the GPU output
+    bit-identical."""
+    s = make_scene("C1")
+    fr = make_frames(s, 0)
+    a = gpu_run(s, [fr])
+    perm = np.array([2, 0, 3, 1])
+    s2 = make_scene("C1")
+    s2.cameras = [s.cameras[i] for i in perm]
+    s2.mu, s2.sigma = s.mu[perm], s.sigma[perm]
+    b = gpu_run(s2, [fr[perm]])
+    assert np.array_equal(a["bits"], b["bits"]) and np.array_equal(a["L"], b["L"])
+
+
+def test_roi_on_off_identical():
+    s = make_scene("C2")
+    fr = [make_frames(s, 0), make_frames(s, 1)]
+    a = gpu_run(s, fr, roi=True)
+    b = gpu_run(s, fr, roi=False)
+    assert np.array_equal(a["bits"], b["bits"]) and np.array_equal(a["L"], b["L"])
+    roi = a["rec"].roi()
+    area = ((roi[:, 1] - roi[:, 0]) * (roi[:, 3] - roi[:, 2])).sum()
+    assert area < s.ncam * 640 * 480
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_zslab_handles_concatenate_to_full(world):
+    """z-slab partition on one GPU: each rank's handle writes exactly its slab's
+    words and log-odds; together they are bit-identical to the 1-handle run."""
+    s = make_scene("C2")
+    fr = [make_frames(s, 0)]
+    full = gpu_run(s, fr)
+    nw = s.grid.nwords
+    plane = s.grid.xlen * s.grid.ylen
+    bits = np.zeros(nw, np.uint32)
+    for r in range(world):
+        part = gpu_run(s, fr, rank=r, world=world)
+        k0, k1 = part["rec"].k0, part["rec"].k1
+        w0, w1 = plane * k0 // 32, plane * k1 // 32
+        bits[w0:w1] = part["bits"][0][w0:w1]
+        assert np.array_equal(part["L"][0], full["L"][0][plane * k0: plane * k1])
+        roi_full = full["rec"].roi()
+        roi = part["rec"].roi()
+        assert ((roi[:, 1] - roi[:, 0]) <= (roi_full[:, 1] - roi_full[:, 0])).all()
+    assert np.array_equal(bits, full["bits"][0])
+
+
+def test_reconstruct_host_matches_device_path():
+    from paper_1311_6811_b200 import from_scene
+    s = make_scene("C2")
+    frames = np.stack([make_frames(s, f) for f in range(11)])
+    dev = gpu_run(s, list(frames))
+    rec = from_scene(s)
+    hf = torch.from_numpy(frames).pin_memory()
+    Lh = torch.empty((11, rec.nslab), dtype=torch.float32).pin_memory()
+    Bh = torch.zeros((11, s.grid.nwords), dtype=torch.int32).pin_memory()
+    rec.reconstruct_host(hf, 11, Lh, Bh)
+    torch.cuda.synchronize()
+    assert np.array_equal(Bh.numpy().view(np.uint32), dev["bits"])
+    assert np.array_equal(Lh.numpy(), dev["L"])
+
+
+# ------------------------------------------------------------------ full sizes, sampled
+
+def _sample_voxels(grid, rng, n_random=1 << 16, every=64):
+    plane = grid.xlen * grid.ylen
+    ks = np.arange(0, grid.zlen, every)
+    rows = np.concatenate([k * plane + rng.integers(0, plane, 4096) for k in ks])
+    return np.unique(np.concatenate([rows, rng.integers(0, grid.nvox, n_random)]))
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_full_size_sampled(name):
+    """C4 (512^3, 16 cams 1920x1080) and C5 (1024^3, 32 cams): the full-size GPU
+    run, checked on a voxel sample (every 64th z-slice x 4096 voxels + 65536
+    random voxels) that the oracle evaluates voxel by voxel, plus an invariant
+    over every voxel (occupied <=> L > logit tau at tau = p_V = 1/2)."""
+    from paper_1311_6811_b200 import from_scene
+    s = make_scene(name)
+    fr = make_frames(s, 0)
+    rec = from_scene(s)
+    L, B = rec.alloc_outputs(1)
+    rec.reconstruct_batch(torch.from_numpy(fr).cuda(), 1, logodds=L, bits=B)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(7)
+    vox = _sample_voxels(s.grid, rng)
+    Lo, post = oracle.fuse_sample(s.P, s.widths, s.heights, s.grid, fr, s.mu, s.sigma, vox,
+                                  nthreads=NTHREADS)
+    vt = torch.from_numpy(vox).cuda()
+    Lg = L[0][vt].cpu().numpy().astype(np.float64)
+    assert np.abs(Lg - Lo).max() <= 1e-4
+    words = B[0][(vt >> 5)].cpu().numpy().view(np.uint32)
+    bits = ((words >> (vox & 31).astype(np.uint32)) & 1).astype(bool)
+    mism = bits != (post > 0.5)
+    assert not (mism & ~(np.abs(post - 0.5) < 1e-4)).any()
+    assert bits.sum() > 0
+    # every voxel: bit set <=> L > 0 (integer compare S > 0 vs float L)
+    shifts = torch.arange(32, device="cuda", dtype=torch.int32)
+    allbits = ((B[0].view(-1, 1) >> shifts) & 1).view(-1)[: s.grid.nvox].bool()
+    assert not bool((allbits & (L[0] < 0)).any()) and not bool((~allbits & (L[0] > 0)).any())
