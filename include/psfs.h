@@ -122,7 +122,7 @@ int psfs_set_background(psfs_handle *h, int32_t cam, int32_t width, int32_t heig
                         const float *mean, const float *sigma);
 
 /* Reconstruct one frame set.  frames: HOST array of ncam DEVICE pointers, each
- * an H_c*W_c*3 uint8 RGB image (row-major, channel-interleaved), 4-byte aligned.
+ * an H_c*W_c*3 uint8 RGB image (row-major, channel-interleaved).
  * logodds: DEVICE, nullable, float per voxel of this handle's slab
  * (xlen*ylen*(k1-k0), x-fastest, slab-relative).  bits: DEVICE, nullable,
  * ceil(xlen*ylen*zlen/32) uint32 words for the FULL grid; this handle writes
@@ -193,6 +193,14 @@ int psfs_kernel_times(psfs_handle *h, double *ms, int64_t *launches, int32_t res
 
 /* Number of kernel launches the last psfs_reconstruct* call enqueued. */
 int psfs_last_launch_count(const psfs_handle *h);
+
+/* 1 if the planner proved the fast reciprocal exact for this grid and rig
+ * (DESIGN.md "Pinned projection"), else 0. */
+int psfs_fast_rcp_enabled(const psfs_handle *h);
+
+/* Test hook: on the current device, count the floats w in [lo, hi) (every bit
+ * pattern) whose fast reciprocal differs from the IEEE RN(1/w).  lo > 0. */
+int psfs_debug_rcp_check(float lo, float hi, int64_t *mismatches);
 
 #ifdef __cplusplus
 }

@@ -13,7 +13,7 @@ constexpr int kQBits = 20;   // Q11.20 fixed point for the per-view term t
 // Stage 1 (per-pixel term) launch description.
 struct S1Cam {
     int32_t W, H;
-    int32_t r0, r1, c0, c1;  // region of interest, half-open; c0, c1 multiples of 4 (VEC path)
+    int32_t r0, r1, c0, c1;  // region of interest, half-open
     int64_t off;             // first pixel of this camera in the concatenated pixel space
 };
 
@@ -22,7 +22,7 @@ struct S1Params {
     const uint8_t *frames[kMaxF][kMaxCam];  // [f][c] device pointers, H*W*3 RGB
     const float *mu;                        // 3 planes of total_px floats
     const float *sg;                        // 3 planes of total_px floats (sigma', floored)
-    int32_t *terms;                         // (off + p) * F + f
+    int32_t *terms;                         // (off + p) * F + f, 32-B aligned
     int64_t total_px;
     double ln_po;    // ln p_O
     double ln_1mpo;  // ln (1 - p_O)
@@ -35,6 +35,8 @@ struct VCam {
     float A[12];   // pre-composed pinned projection matrix, row-major 3x4
     int32_t W, H;
     int64_t off;   // pixel offset of this camera's term image
+    int32_t zidx;  // index (relative to off) of the all-zero pixel, total_px - off
+    int32_t pad;
 };
 
 struct VParams {
@@ -45,13 +47,15 @@ struct VParams {
     int32_t xlen, ylen, k0, k1;
     int32_t ncam;
     int32_t Tq;              // occupied iff S > Tq
-    int32_t aligned;         // xlen % 32 == 0: one whole word per warp row
+    int32_t byte_aligned;    // xlen % 8 == 0: each warp row is one whole byte
+    int32_t fast_rcp;        // every w over the grid is <= 0 or in [2^-60, 2^60]
     double logit_pv;
 };
 
 // Launchers (psfs_kernels.cu).  Return the cudaError_t of the launch.
-cudaError_t launch_likelihood(const S1Params &p, int F, bool vec4, int max_rows_px,
-                              cudaStream_t s);
-cudaError_t launch_voxel(const VParams &p, int F, bool want_logodds, cudaStream_t s);
+cudaError_t launch_likelihood(const S1Params &p, int F, int max_roi_px, cudaStream_t s);
+cudaError_t launch_voxel(const VParams &p, int F, cudaStream_t s);
+cudaError_t launch_rcp_check(uint32_t lo_bits, uint32_t hi_bits, unsigned long long *bad,
+                             cudaStream_t s);
 
 }  // namespace psfs

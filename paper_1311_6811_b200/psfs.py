@@ -30,7 +30,8 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_reconstruct", "psfs_reconstruct_batch", "psfs_reconstruct_host", "psfs_destroy",
            "psfs_status_string", "psfs_last_error", "psfs_slab", "psfs_debug_matrices",
            "psfs_debug_terms", "psfs_debug_roi", "psfs_set_roi_enabled", "psfs_set_max_fuse",
-           "psfs_last_launch_count", "psfs_set_profiling", "psfs_kernel_times"]
+           "psfs_last_launch_count", "psfs_set_profiling", "psfs_kernel_times",
+           "psfs_fast_rcp_enabled", "psfs_debug_rcp_check"]
 
 
 class PsfsError(RuntimeError):
@@ -88,6 +89,8 @@ def lib():
         L.psfs_last_launch_count.argtypes = [vp]
         L.psfs_set_profiling.argtypes = [vp, i32]
         L.psfs_kernel_times.argtypes = [vp, vp, vp, i32]
+        L.psfs_fast_rcp_enabled.argtypes = [vp]
+        L.psfs_debug_rcp_check.argtypes = [C.c_float, C.c_float, C.POINTER(C.c_int64)]
         _lib = L
     return _lib
 
@@ -325,8 +328,21 @@ class Reconstructor:
         return {"k_likelihood": (float(ms[0]), int(n[0])), "k_voxel": (float(ms[1]), int(n[1]))}
 
     @property
+    def fast_rcp(self) -> bool:
+        return bool(lib().psfs_fast_rcp_enabled(self._h))
+
+    @property
     def last_launch_count(self):
         return int(lib().psfs_last_launch_count(self._h))
+
+
+def debug_rcp_check(lo: float, hi: float) -> int:
+    """Mismatches between the fast reciprocal and RN(1/w) over every float in [lo, hi)."""
+    n = C.c_int64()
+    rc = lib().psfs_debug_rcp_check(float(lo), float(hi), C.byref(n))
+    if rc != PSFS_OK:
+        raise PsfsError(rc, "psfs_debug_rcp_check")
+    return int(n.value)
 
 
 def from_scene(scene, params=None, device=None, rank=0, world=1) -> Reconstructor:

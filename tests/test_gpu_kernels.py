@@ -1,0 +1,52 @@
+"""GPU checks of kernel building blocks that parity tests cannot isolate."""
+import numpy as np
+import pytest
+
+import oracle
+from synth.scene import Grid, look_at_camera, make_frames, make_scene, ring_rig
+from tests.helpers import assert_parity, gpu_run
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1311_6811_b200 import build
+    build.build()
+
+
+def test_fast_reciprocal_is_ieee_rn_over_planner_range():
+    """The planner enables the MUFU+Newton reciprocal only when every in-front w
+    lies in [2^-60, 2^60]; over every float of that range it must equal
+    __frcp_rn (IEEE RN(1/w)) bit for bit."""
+    from paper_1311_6811_b200.psfs import debug_rcp_check
+    assert debug_rcp_check(2.0 ** -60, 2.0 ** 60) == 0
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_planner_enables_fast_reciprocal_for_ring_rigs(name):
+    from paper_1311_6811_b200 import Reconstructor
+    s = make_scene(name) if name in ("C1", "C2") else None
+    from synth.scene import CONFIGS, cube_grid
+    cfg = CONFIGS[name]
+    cams = ring_rig(cfg["rings"], cfg["W"], cfg["H"])
+    rec = Reconstructor(cube_grid(cfg["n"]))
+    rec.set_cameras(np.stack([c.P for c in cams]), [c.width for c in cams],
+                    [c.height for c in cams])
+    assert rec.fast_rcp
+
+
+def test_camera_inside_grid_uses_exact_reciprocal_and_matches_oracle():
+    """A camera whose principal plane cuts the grid (w changes sign inside it):
+    the planner must fall back to __frcp_rn; parity with the oracle holds,
+    including voxels behind that camera."""
+    s = make_scene("C1")
+    inner = look_at_camera((0.0, -300.0, 1000.0), (0.0, 3000.0, 1000.0), 64, 48)
+    s.cameras = s.cameras[:3] + [inner]
+    g = gpu_run(s, [make_frames(s, 0)])
+    assert not g["rec"].fast_rcp
+    orc = oracle.scene_reconstruct(s, make_frames(s, 0))
+    assert_parity(g["L"][0], g["bits"][0], orc, s.grid.nvox)
