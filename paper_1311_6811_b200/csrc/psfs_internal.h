@@ -13,21 +13,27 @@ constexpr int kQBits = 20;   // Q11.20 fixed point for the per-view term t
 // Stage 1 (per-pixel term) launch description.
 struct S1Cam {
     int32_t W, H;
-    int32_t r0, r1, c0, c1;  // region of interest, half-open
+    int32_t r0, r1, c0, c1;  // region of interest, half-open (c0, c1 multiples of 16 on the TMA path)
     int64_t off;             // first pixel of this camera in the concatenated pixel space
+    int32_t seg_begin;       // TMA path: first segment index of this camera
+    int32_t segs_per_row;    // TMA path: ceil((c1 - c0) / kSeg)
 };
+
+constexpr int kSeg = 256;  // pixels per TMA segment (one row chunk) = threads per block
 
 struct S1Params {
     S1Cam cam[kMaxCam];
     const uint8_t *frames[kMaxF][kMaxCam];  // [f][c] device pointers, H*W*3 RGB
     const float *mu;                        // 3 planes of total_px floats
     const float *sg;                        // 3 planes of total_px floats (sigma', floored)
+    const double *K;                        // total_px: 24 ln 2 - 1.5 ln 2pi - ln(s0 s1 s2)
     int32_t *terms;                         // (off + p) * F + f, 32-B aligned
     int64_t total_px;
     double ln_po;    // ln p_O
     double ln_1mpo;  // ln (1 - p_O)
     double c0;       // -1.5 ln(2 pi) - ln U = 24 ln 2 - 1.5 ln(2 pi)
     int32_t ncam;
+    int32_t nseg;    // TMA path: total segments over all cameras
 };
 
 // Stage 2 (voxel) launch description.
@@ -50,11 +56,19 @@ struct VParams {
     int32_t byte_aligned;    // xlen % 8 == 0: each warp row is one whole byte
     int32_t fast_rcp;        // every w over the grid is <= 0 or in [2^-60, 2^60]
     double logit_pv;
+    unsigned long long *tile_counter;  // persistent scheduling: monotone per handle
+    long long tile_base;               // counter value at this launch's start
+    int32_t ntiles;
 };
 
+constexpr int kKZ = 4;  // z-slices per stage-2 tile
+
 // Launchers (psfs_kernels.cu).  Return the cudaError_t of the launch.
-cudaError_t launch_likelihood(const S1Params &p, int F, int max_roi_px, cudaStream_t s);
-cudaError_t launch_voxel(const VParams &p, int F, cudaStream_t s);
+cudaError_t launch_likelihood(const S1Params &p, int F, int max_roi_px, bool tma, cudaStream_t s);
+cudaError_t launch_prep_model(const float *sg, double *K, int64_t total_px, int64_t begin,
+                              int64_t n, double c0, cudaStream_t s);
+cudaError_t launch_voxel(const VParams &p, int F, cudaStream_t s, int *nblocks);
+int voxel_tiles(int xlen, int ylen, int k0, int k1);
 cudaError_t launch_rcp_check(uint32_t lo_bits, uint32_t hi_bits, unsigned long long *bad,
                              cudaStream_t s);
 

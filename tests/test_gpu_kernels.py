@@ -50,3 +50,28 @@ def test_camera_inside_grid_uses_exact_reciprocal_and_matches_oracle():
     assert not g["rec"].fast_rcp
     orc = oracle.scene_reconstruct(s, make_frames(s, 0))
     assert_parity(g["L"][0], g["bits"][0], orc, s.grid.nvox)
+
+
+def test_stage1_tma_ring_equals_generic_path():
+    """Stage 1 takes the TMA (cp.async.bulk + mbarrier) ring when frames are
+    16-byte aligned and W % 16 == 0, else the generic kernel; both must give
+    bit-identical terms and outputs."""
+    from paper_1311_6811_b200 import from_scene
+    s = make_scene("C2")
+    frames = np.stack([make_frames(s, f) for f in range(8)])
+    rec = from_scene(s)
+    n = frames.size
+    aligned = torch.from_numpy(frames).cuda()
+    raw = torch.empty(n + 4, dtype=torch.uint8, device="cuda")
+    raw[4:].copy_(aligned.view(-1))
+    shifted = raw[4:].view(frames.shape)            # 4-byte misaligned -> generic kernel
+    assert shifted.data_ptr() % 16 == 4
+    La, Ba = rec.alloc_outputs(8)
+    Lb, Bb = rec.alloc_outputs(8)
+    rec.reconstruct_batch(aligned, 8, logodds=La, bits=Ba)
+    rec.reconstruct_batch(shifted, 8, logodds=Lb, bits=Bb)
+    torch.cuda.synchronize()
+    assert torch.equal(Ba, Bb) and torch.equal(La, Lb)
+    ta = rec.debug_terms(aligned[0])
+    tb = rec.debug_terms(shifted[0])
+    assert torch.equal(ta, tb)
