@@ -198,6 +198,11 @@ int psfs_last_launch_count(const psfs_handle *h);
  * (DESIGN.md "Pinned projection"), else 0. */
 int psfs_fast_rcp_enabled(const psfs_handle *h);
 
+/* Microbenchmark on the current device: L1 load bandwidth (bytes/s) of fully
+ * coalesced 128-bit loads from an L1-resident window, the peak the stage-2
+ * gather is compared against. */
+int psfs_probe_l1_bandwidth(double *bytes_per_s);
+
 /* Test hook: on the current device, count the floats w in [lo, hi) (every bit
  * pattern) whose fast reciprocal differs from the IEEE RN(1/w).  lo > 0. */
 int psfs_debug_rcp_check(float lo, float hi, int64_t *mismatches);

@@ -10,6 +10,17 @@ constexpr int kMaxCam = 64;  // == PSFS_MAX_CAMERAS
 constexpr int kMaxF = 8;     // == PSFS_MAX_BATCH
 constexpr int kQBits = 20;   // Q11.20 fixed point for the per-view term t
 
+// Background model of one pixel as stored on the device (set once by
+// psfs_set_background; K filled by k_prep_model): 32 bytes, so a row segment of
+// the model is one contiguous block (one bulk copy) and a warp's 32 records are
+// 1 KB of coalesced loads.
+struct ModelPx {
+    float mu[3];  // mean per channel
+    float sg[3];  // sigma' = max(sigma, sigma_floor) per channel (R#6)
+    double K;     // 24 ln 2 - 1.5 ln(2 pi) - ln(sg0 sg1 sg2)
+};
+static_assert(sizeof(ModelPx) == 32, "ModelPx must be 32 bytes");
+
 // Stage 1 (per-pixel term) launch description.
 struct S1Cam {
     int32_t W, H;
@@ -19,14 +30,12 @@ struct S1Cam {
     int32_t segs_per_row;    // TMA path: ceil((c1 - c0) / kSeg)
 };
 
-constexpr int kSeg = 256;  // pixels per TMA segment (one row chunk) = threads per block
+constexpr int kSeg = 512;  // pixels per TMA segment (one row chunk) = consumer threads per block
 
 struct S1Params {
     S1Cam cam[kMaxCam];
     const uint8_t *frames[kMaxF][kMaxCam];  // [f][c] device pointers, H*W*3 RGB
-    const float *mu;                        // 3 planes of total_px floats
-    const float *sg;                        // 3 planes of total_px floats (sigma', floored)
-    const double *K;                        // total_px: 24 ln 2 - 1.5 ln 2pi - ln(s0 s1 s2)
+    const struct ModelPx *model;            // total_px records (AoS, 32 B each)
     int32_t *terms;                         // (off + p) * F + f, 32-B aligned
     int64_t total_px;
     double ln_po;    // ln p_O
@@ -65,10 +74,10 @@ constexpr int kKZ = 4;  // z-slices per stage-2 tile
 
 // Launchers (psfs_kernels.cu).  Return the cudaError_t of the launch.
 cudaError_t launch_likelihood(const S1Params &p, int F, int max_roi_px, bool tma, cudaStream_t s);
-cudaError_t launch_prep_model(const float *sg, double *K, int64_t total_px, int64_t begin,
-                              int64_t n, double c0, cudaStream_t s);
+cudaError_t launch_prep_model(ModelPx *model, int64_t begin, int64_t n, double c0, cudaStream_t s);
 cudaError_t launch_voxel(const VParams &p, int F, cudaStream_t s, int *nblocks);
 int voxel_tiles(int xlen, int ylen, int k0, int k1);
+cudaError_t launch_l1_probe(const void *buf, int blocks, int iters, int *out, cudaStream_t s);
 cudaError_t launch_rcp_check(uint32_t lo_bits, uint32_t hi_bits, unsigned long long *bad,
                              cudaStream_t s);
 

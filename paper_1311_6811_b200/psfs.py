@@ -31,7 +31,7 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_status_string", "psfs_last_error", "psfs_slab", "psfs_debug_matrices",
            "psfs_debug_terms", "psfs_debug_roi", "psfs_set_roi_enabled", "psfs_set_max_fuse",
            "psfs_last_launch_count", "psfs_set_profiling", "psfs_kernel_times",
-           "psfs_fast_rcp_enabled", "psfs_debug_rcp_check"]
+           "psfs_fast_rcp_enabled", "psfs_debug_rcp_check", "psfs_probe_l1_bandwidth"]
 
 
 class PsfsError(RuntimeError):
@@ -91,6 +91,7 @@ def lib():
         L.psfs_kernel_times.argtypes = [vp, vp, vp, i32]
         L.psfs_fast_rcp_enabled.argtypes = [vp]
         L.psfs_debug_rcp_check.argtypes = [C.c_float, C.c_float, C.POINTER(C.c_int64)]
+        L.psfs_probe_l1_bandwidth.argtypes = [C.POINTER(C.c_double)]
         _lib = L
     return _lib
 
@@ -343,6 +344,15 @@ def debug_rcp_check(lo: float, hi: float) -> int:
     if rc != PSFS_OK:
         raise PsfsError(rc, "psfs_debug_rcp_check")
     return int(n.value)
+
+
+def probe_l1_bandwidth() -> float:
+    """Measured L1 load bandwidth (bytes/s) of the current device."""
+    v = C.c_double()
+    rc = lib().psfs_probe_l1_bandwidth(C.byref(v))
+    if rc != PSFS_OK:
+        raise PsfsError(rc, "psfs_probe_l1_bandwidth")
+    return float(v.value)
 
 
 def from_scene(scene, params=None, device=None, rank=0, world=1) -> Reconstructor:
