@@ -25,7 +25,9 @@ static_assert(sizeof(ModelPx) == 32, "ModelPx must be 32 bytes");
 struct S1Cam {
     int32_t W, H;
     int32_t r0, r1, c0, c1;  // region of interest, half-open (c0, c1 multiples of 16 on the TMA path)
-    int64_t off;             // first pixel of this camera in the concatenated pixel space
+    int64_t off;             // first pixel of this camera in the concatenated pixel space (model)
+    int64_t toff;            // first pixel of this camera's term image
+    int32_t tstride;         // term image row stride in pixels (W + 1: padded, or W for debug)
     int32_t seg_begin;       // TMA path: first segment index of this camera
     int32_t segs_per_row;    // TMA path: ceil((c1 - c0) / kSeg)
 };
@@ -46,12 +48,14 @@ struct S1Params {
 };
 
 // Stage 2 (voxel) launch description.
+// Term images are stored padded to (W+1) x (H+1) pixels: the extra column W and
+// row H are all-zero terms (t = 0, the out-of-view contribution, R#12), so an
+// out-of-view projection is clamped into the pad instead of branched on.
 struct VCam {
-    float A[12];   // pre-composed pinned projection matrix, row-major 3x4
+    float A[12];    // pre-composed pinned projection matrix, row-major 3x4
     int32_t W, H;
-    int64_t off;   // pixel offset of this camera's term image
-    int32_t zidx;  // index (relative to off) of the all-zero pixel, total_px - off
-    int32_t pad;
+    uint32_t toff;  // first pixel of this camera's padded term image (< 2^28)
+    uint32_t Wp;    // padded row stride W + 1
 };
 
 struct VParams {
