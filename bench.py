@@ -44,6 +44,10 @@ def parse():
     ap.add_argument("--pool", type=int, default=16, help="distinct frame sets cycled")
     ap.add_argument("--fuse", type=int, default=8, help="frames fused per kernel pass")
     ap.add_argument("--config", default="C2")
+    ap.add_argument("--ty", type=int, default=1)
+    ap.add_argument("--kz", type=int, default=4)
+    ap.add_argument("--stage1", type=int, default=0, choices=[0, 1, 2],
+                    help="stage-1 kernel: 0 one pixel per thread, 1 TMA ring, 2 pipelined")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -122,6 +126,37 @@ def make_workload(config, n_distinct, seed_offset=0):
     s = make_scene(config)
     frames = np.stack([make_frames(s, seed_offset + f) for f in range(n_distinct)])
     return s, frames
+
+
+def gather_sectors(scene, F):
+    """Algorithmic L1 sector count of one k_voxel launch: for every warp (8 x 4
+    voxels in x, y at one z), camera and slice, the number of distinct pixels the
+    32 voxel centres project to (each pixel's F terms are one 32-byte sector for
+    F = 8).  Nearest pixel in double precision (the pinned FP32 pixel differs on
+    ~0.1 % of voxel-cameras, irrelevant for a count)."""
+    g = scene.grid
+    i = np.arange(g.xlen)
+    j = np.arange(g.ylen)
+    X = g.origin[0] + g.spacing * (i + 0.5)
+    Y = g.origin[1] + g.spacing * (j + 0.5)
+    total = 0
+    for c in range(scene.ncam):
+        P = scene.P[c]
+        for k in range(g.zlen):
+            Z = g.origin[2] + g.spacing * (k + 0.5)
+            x = P[0, 0] * X[None, :] + P[0, 1] * Y[:, None] + P[0, 2] * Z + P[0, 3]
+            y = P[1, 0] * X[None, :] + P[1, 1] * Y[:, None] + P[1, 2] * Z + P[1, 3]
+            w = P[2, 0] * X[None, :] + P[2, 1] * Y[:, None] + P[2, 2] * Z + P[2, 3]
+            u = np.floor(x / w + 0.5).astype(np.int64)
+            v = np.floor(y / w + 0.5).astype(np.int64)
+            inview = (w > 0) & (u >= 0) & (u < scene.widths[c]) & (v >= 0) & (v < scene.heights[c])
+            pix = np.where(inview, v * (scene.widths[c] + 1) + u, -1)   # -1: the zero pad
+            # [ylen, xlen] -> warps of 4 rows x 8 columns
+            t = pix.reshape(g.ylen // 4, 4, g.xlen // 8, 8).transpose(0, 2, 1, 3).reshape(-1, 32)
+            t = np.sort(t, axis=1)
+            total += int((1 + (np.diff(t, axis=1) != 0).sum(axis=1)).sum())
+    sector_bytes = 32 if F == 8 else 4 * F
+    return total, total * sector_bytes
 
 
 def cpu_baseline(scene, frames, seconds, nthreads):
@@ -210,6 +245,8 @@ def run_ours(args):
     scene, frames = make_workload(args.config, pool, seed_offset=rank * pool)
     rec = from_scene(scene, device=local)
     rec.set_max_fuse(args.fuse)
+    rec.set_stage1_path(args.stage1)
+    rec.set_voxel_tile(args.ty, args.kz)
     frames_dev = torch.from_numpy(frames).to(dev)
     L, Bits = rec.alloc_outputs(B, logodds=False, bits=True)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
@@ -292,22 +329,31 @@ def run_ours(args):
     # the planned pixel rectangle
     s1_bytes = roi_px * (24 + 7 * F)
     s1_avg_s = (l_ms / max(l_n, 1)) / 1e3
-    # stage 2 algorithmic gather bytes per launch: every voxel-camera-frame reads
-    # the 4-byte term of the pixel its centre projects to
-    s2_bytes = nvox * ncam * F * 4
+    # stage 2: the gather is bound by the L1TEX data pipe, one 32-byte sector per
+    # clock per SM for 32-byte-per-lane loads (ncu: l1tex__data_pipe_lsu_wavefronts
+    # equals the sectors requested); algorithmic sectors = distinct pixels per
+    # warp-gather for this tiling (gather_sectors), peak = 1 sector/clk/SM
     v_avg_s = (v_ms / max(v_n, 1)) / 1e3
+    sectors, s2_bytes = gather_sectors(scene, F)
+    sm_clk = (clocks or {}).get("sm_mhz") or float(peaks.get("sm_max_mhz", 1965.0))
+    import torch as _t
+    nsm = _t.cuda.get_device_properties(dev).multi_processor_count
+    l1_sector_peak = nsm * sm_clk * 1e6 * 32 / 1e9
     per_kernel = {
         "k_likelihood": {
             "bound": "hbm", "achieved": s1_bytes / s1_avg_s / 1e9, "peak": hbm_peak,
             "unit": "GB/s", "peak_source": hbm_src, "algorithmic_bytes_per_launch": s1_bytes,
             "avg_launch_us": s1_avg_s * 1e6, "traffic": traffic.get("k_likelihood")},
         "k_voxel": {
-            "bound": "l1", "achieved": s2_bytes / v_avg_s / 1e9, "peak": l1_peak,
+            "bound": "l1", "achieved": s2_bytes / v_avg_s / 1e9, "peak": l1_sector_peak,
             "unit": "GB/s",
-            "peak_source": "measured in this run: psfs_probe_l1_bandwidth (coalesced 128-bit "
-                           "loads, L1-resident), the data-pipe peak the term gathers share",
-            "algorithmic_bytes_per_launch": s2_bytes, "avg_launch_us": v_avg_s * 1e6,
-            "voxel_cam_frames_per_s": nvox * ncam * F / v_avg_s, "traffic": traffic.get("k_voxel")},
+            "peak_source": f"derived: {nsm} SMs x 1 L1TEX data-pipe wavefront/clk x 32-byte "
+                           f"sector x {sm_clk:.0f} MHz (median SM clock of this run); "
+                           "DESIGN.md section 8",
+            "algorithmic_bytes_per_launch": s2_bytes, "sectors_per_launch": sectors,
+            "avg_launch_us": v_avg_s * 1e6,
+            "voxel_cam_frames_per_s": nvox * ncam * F / v_avg_s, "traffic": traffic.get("k_voxel"),
+            "l1_load_probe_gbs": l1_peak},
     }
     for v in per_kernel.values():
         v["frac"] = v["achieved"] / v["peak"]

@@ -180,6 +180,16 @@ int psfs_debug_roi(const psfs_handle *h, int32_t *out);
 /* Enable/disable the ROI restriction of stage 1 (default on). */
 int psfs_set_roi_enabled(psfs_handle *h, int32_t enabled);
 
+/* Stage-1 kernel: 0 = one pixel per thread, all loads first (default),
+ * 1 = TMA bulk-copy ring (falls back to 0 when some W % 16 != 0 or a frame
+ * pointer is not 16-byte aligned), 2 = software-pipelined persistent kernel.
+ * All three give bit-identical terms (DESIGN.md §8 has the measurements). */
+int psfs_set_stage1_path(psfs_handle *h, int32_t path);
+
+/* Stage-2 tile shape: 32 x 8*ty voxel columns (ty = 1 or 4, default 1) by kz
+ * z-slices (1..64, default 4).  Results are bit-identical for every shape. */
+int psfs_set_voxel_tile(psfs_handle *h, int32_t ty, int32_t kz);
+
 /* Cap the number of frames fused into one pass (1, 2, 4 or 8; default 8). */
 int psfs_set_max_fuse(psfs_handle *h, int32_t fmax);
 

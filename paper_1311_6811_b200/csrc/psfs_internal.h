@@ -30,6 +30,8 @@ struct S1Cam {
     int32_t tstride;         // term image row stride in pixels (W + 1: padded, or W for debug)
     int32_t seg_begin;       // TMA path: first segment index of this camera
     int32_t segs_per_row;    // TMA path: ceil((c1 - c0) / kSeg)
+    int32_t q_begin;         // pipelined path: first ROI pixel index of this camera
+    int32_t pad_;
 };
 
 constexpr int kSeg = 512;  // pixels per TMA segment (one row chunk) = consumer threads per block
@@ -45,6 +47,7 @@ struct S1Params {
     double c0;       // -1.5 ln(2 pi) - ln U = 24 ln 2 - 1.5 ln(2 pi)
     int32_t ncam;
     int32_t nseg;    // TMA path: total segments over all cameras
+    int32_t nq;      // pipelined path: total ROI pixels over all cameras
 };
 
 // Stage 2 (voxel) launch description.
@@ -72,15 +75,15 @@ struct VParams {
     unsigned long long *tile_counter;  // persistent scheduling: monotone per handle
     long long tile_base;               // counter value at this launch's start
     int32_t ntiles;
+    int32_t ty;                        // y sub-tiles per warp (1 or 4): tile = 32 x 8ty columns
+    int32_t kz;                        // z-slices per tile
 };
 
-constexpr int kKZ = 4;  // z-slices per stage-2 tile
-
 // Launchers (psfs_kernels.cu).  Return the cudaError_t of the launch.
-cudaError_t launch_likelihood(const S1Params &p, int F, int max_roi_px, bool tma, cudaStream_t s);
+cudaError_t launch_likelihood(const S1Params &p, int F, int max_roi_px, int path, cudaStream_t s);
 cudaError_t launch_prep_model(ModelPx *model, int64_t begin, int64_t n, double c0, cudaStream_t s);
 cudaError_t launch_voxel(const VParams &p, int F, cudaStream_t s, int *nblocks);
-int voxel_tiles(int xlen, int ylen, int k0, int k1);
+int voxel_tiles(int xlen, int ylen, int k0, int k1, int ty, int kz);
 cudaError_t launch_l1_probe(const void *buf, int blocks, int iters, int *out, cudaStream_t s);
 cudaError_t launch_rcp_check(uint32_t lo_bits, uint32_t hi_bits, unsigned long long *bad,
                              cudaStream_t s);

@@ -17,7 +17,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpsfs.so")
+# PSFS_LIB overrides the library (A/B experiments with variant builds only)
+LIB_PATH = os.environ.get("PSFS_LIB", os.path.join(_HERE, "libpsfs.so"))
 
 PSFS_OK = 0
 STATUS = {0: "PSFS_OK", 1: "PSFS_EINVAL", 2: "PSFS_EDEGENERATE", 3: "PSFS_EDIM", 4: "PSFS_ECOUNT",
@@ -31,7 +32,8 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_status_string", "psfs_last_error", "psfs_slab", "psfs_debug_matrices",
            "psfs_debug_terms", "psfs_debug_roi", "psfs_set_roi_enabled", "psfs_set_max_fuse",
            "psfs_last_launch_count", "psfs_set_profiling", "psfs_kernel_times",
-           "psfs_fast_rcp_enabled", "psfs_debug_rcp_check", "psfs_probe_l1_bandwidth"]
+           "psfs_fast_rcp_enabled", "psfs_debug_rcp_check", "psfs_probe_l1_bandwidth",
+           "psfs_set_stage1_path", "psfs_set_voxel_tile"]
 
 
 class PsfsError(RuntimeError):
@@ -86,6 +88,8 @@ def lib():
         L.psfs_debug_roi.argtypes = [vp, vp]
         L.psfs_set_roi_enabled.argtypes = [vp, i32]
         L.psfs_set_max_fuse.argtypes = [vp, i32]
+        L.psfs_set_stage1_path.argtypes = [vp, i32]
+        L.psfs_set_voxel_tile.argtypes = [vp, i32, i32]
         L.psfs_last_launch_count.argtypes = [vp]
         L.psfs_set_profiling.argtypes = [vp, i32]
         L.psfs_kernel_times.argtypes = [vp, vp, vp, i32]
@@ -208,6 +212,13 @@ class Reconstructor:
 
     def set_max_fuse(self, fmax: int):
         self._check(lib().psfs_set_max_fuse(self._h, int(fmax)), "psfs_set_max_fuse")
+
+    def set_voxel_tile(self, ty: int, kz: int):
+        self._check(lib().psfs_set_voxel_tile(self._h, int(ty), int(kz)), "psfs_set_voxel_tile")
+
+    def set_stage1_path(self, path: int):
+        """2 pipelined (default), 1 TMA ring, 0 one pixel per thread."""
+        self._check(lib().psfs_set_stage1_path(self._h, int(path)), "psfs_set_stage1_path")
 
     def set_roi_enabled(self, on: bool):
         self._check(lib().psfs_set_roi_enabled(self._h, int(bool(on))), "psfs_set_roi_enabled")

@@ -52,14 +52,18 @@ def test_camera_inside_grid_uses_exact_reciprocal_and_matches_oracle():
     assert_parity(g["L"][0], g["bits"][0], orc, s.grid.nvox)
 
 
-def test_stage1_tma_ring_equals_generic_path():
-    """Stage 1 takes the TMA (cp.async.bulk + mbarrier) ring when frames are
-    16-byte aligned and W % 16 == 0, else the generic kernel; both must give
-    bit-identical terms and outputs."""
+@pytest.mark.parametrize("path", [0, 2])
+def test_stage1_paths_bit_identical(path):
+    """The three stage-1 kernels (TMA ring with cp.async.bulk + mbarrier, used
+    when frames are 16-byte aligned and W % 16 == 0; pipelined persistent; one
+    pixel per thread) give bit-identical terms and outputs."""
     from paper_1311_6811_b200 import from_scene
     s = make_scene("C2")
     frames = np.stack([make_frames(s, f) for f in range(8)])
     rec = from_scene(s)
+    ref = from_scene(s)
+    ref.set_stage1_path(1)
+    rec.set_stage1_path(path)
     n = frames.size
     aligned = torch.from_numpy(frames).cuda()
     raw = torch.empty(n + 4, dtype=torch.uint8, device="cuda")
@@ -68,10 +72,12 @@ def test_stage1_tma_ring_equals_generic_path():
     assert shifted.data_ptr() % 16 == 4
     La, Ba = rec.alloc_outputs(8)
     Lb, Bb = rec.alloc_outputs(8)
-    rec.reconstruct_batch(aligned, 8, logodds=La, bits=Ba)
-    rec.reconstruct_batch(shifted, 8, logodds=Lb, bits=Bb)
+    Lc, Bc = rec.alloc_outputs(8)
+    ref.reconstruct_batch(aligned, 8, logodds=La, bits=Ba)      # TMA ring
+    ref.reconstruct_batch(shifted, 8, logodds=Lb, bits=Bb)      # misaligned: path 0
+    rec.reconstruct_batch(aligned, 8, logodds=Lc, bits=Bc)
     torch.cuda.synchronize()
     assert torch.equal(Ba, Bb) and torch.equal(La, Lb)
-    ta = rec.debug_terms(aligned[0])
-    tb = rec.debug_terms(shifted[0])
-    assert torch.equal(ta, tb)
+    assert torch.equal(Ba, Bc) and torch.equal(La, Lc)
+    for r in (rec, ref):
+        assert torch.equal(r.debug_terms(aligned[0]), ref.debug_terms(shifted[0]))
