@@ -46,8 +46,9 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--ty", type=int, default=1)
     ap.add_argument("--kz", type=int, default=4)
-    ap.add_argument("--stage1", type=int, default=0, choices=[0, 1, 2],
-                    help="stage-1 kernel: 0 one pixel per thread, 1 TMA ring, 2 pipelined")
+    ap.add_argument("--stage1", type=int, default=0, choices=[0, 1, 2, 3, 4],
+                    help="stage-1 kernel: 0 one pixel/thread, 1 TMA ring, 2 pipelined, "
+                         "3 four pixels/thread, 4 warp-row loads (A/B experiments)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

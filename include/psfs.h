@@ -180,10 +180,12 @@ int psfs_debug_roi(const psfs_handle *h, int32_t *out);
 /* Enable/disable the ROI restriction of stage 1 (default on). */
 int psfs_set_roi_enabled(psfs_handle *h, int32_t enabled);
 
-/* Stage-1 kernel: 0 = one pixel per thread, all loads first (default),
- * 1 = TMA bulk-copy ring (falls back to 0 when some W % 16 != 0 or a frame
- * pointer is not 16-byte aligned), 2 = software-pipelined persistent kernel.
- * All three give bit-identical terms (DESIGN.md §8 has the measurements). */
+/* Stage-1 kernel: 0 = one pixel per thread (default); 1 = TMA bulk-copy ring
+ * (needs every W % 16 == 0 and 16-byte aligned frames); 2 = software-pipelined
+ * persistent kernel; 3 = four pixels per thread (W % 4, 4-byte aligned frames);
+ * 4 = warp-row coalesced image loads with shuffles (W % 32, 4-byte aligned).
+ * A path whose requirement fails falls back to 0.  All give bit-identical terms
+ * (DESIGN.md §8 has the measurements that made 0 the default). */
 int psfs_set_stage1_path(psfs_handle *h, int32_t path);
 
 /* Stage-2 tile shape: 32 x 8*ty voxel columns (ty = 1 or 4, default 1) by kz

@@ -217,7 +217,8 @@ class Reconstructor:
         self._check(lib().psfs_set_voxel_tile(self._h, int(ty), int(kz)), "psfs_set_voxel_tile")
 
     def set_stage1_path(self, path: int):
-        """2 pipelined (default), 1 TMA ring, 0 one pixel per thread."""
+        """0 one pixel/thread (default), 1 TMA ring, 2 pipelined, 3 four pixels/thread,
+        4 warp-row loads (see include/psfs.h)."""
         self._check(lib().psfs_set_stage1_path(self._h, int(path)), "psfs_set_stage1_path")
 
     def set_roi_enabled(self, on: bool):

@@ -52,7 +52,7 @@ def test_camera_inside_grid_uses_exact_reciprocal_and_matches_oracle():
     assert_parity(g["L"][0], g["bits"][0], orc, s.grid.nvox)
 
 
-@pytest.mark.parametrize("path", [0, 2])
+@pytest.mark.parametrize("path", [0, 2, 3, 4])
 def test_stage1_paths_bit_identical(path):
     """The three stage-1 kernels (TMA ring with cp.async.bulk + mbarrier, used
     when frames are 16-byte aligned and W % 16 == 0; pipelined persistent; one
