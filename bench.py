@@ -40,8 +40,11 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--batch", type=int, default=8, help="frames per step per GPU")
-    ap.add_argument("--pool", type=int, default=16, help="distinct frame sets cycled")
+    ap.add_argument("--batch", type=int, default=32, help="frames per step per GPU")
+    ap.add_argument("--pool", type=int, default=32, help="distinct frame sets cycled")
+    ap.add_argument("--overlap", type=int, default=0,
+                    help="overlap stage 1 of group g+1 with stage 2 of group g; value = k_voxel "
+                         "blocks/SM cap (0: none); -1: serial schedule")
     ap.add_argument("--fuse", type=int, default=8, help="frames fused per kernel pass")
     ap.add_argument("--config", default="C2")
     ap.add_argument("--ty", type=int, default=1)
@@ -248,6 +251,7 @@ def run_ours(args):
     rec.set_max_fuse(args.fuse)
     rec.set_stage1_path(args.stage1)
     rec.set_voxel_tile(args.ty, args.kz)
+    rec.set_overlap(args.overlap >= 0, max(args.overlap, 0))
     frames_dev = torch.from_numpy(frames).to(dev)
     L, Bits = rec.alloc_outputs(B, logodds=False, bits=True)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
@@ -420,6 +424,9 @@ def run_ours(args):
                        "grid": [scene.grid.xlen, scene.grid.ylen, scene.grid.zlen],
                        "cameras": ncam, "image": [int(scene.widths[0]), int(scene.heights[0])],
                        "distinct_frame_sets": pool, "parallelism": f"frame-parallel x{world}",
+                       "schedule": ("stage 1 of group g+1 overlapped with stage 2 of group g"
+                                    + (f" (k_voxel capped at {args.overlap} blocks/SM)" if args.overlap > 0 else "")
+                                    if args.overlap >= 0 else "serial"),
                        "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the step events)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,

@@ -188,6 +188,13 @@ int psfs_set_roi_enabled(psfs_handle *h, int32_t enabled);
  * (DESIGN.md §8 has the measurements that made 0 the default). */
 int psfs_set_stage1_path(psfs_handle *h, int32_t path);
 
+/* Overlapped batches (default on): with more than one frame group in a
+ * psfs_reconstruct_batch call, stage 1 of group g+1 runs on an internal stream
+ * beside stage 2 of group g (two term buffers); voxel_blocks_per_sm > 0 caps
+ * k_voxel's resident blocks per SM to leave room for stage-1 blocks (default 0:
+ * no cap, the measured best on B200).  Results are bit-identical either way. */
+int psfs_set_overlap(psfs_handle *h, int32_t enabled, int32_t voxel_blocks_per_sm);
+
 /* Stage-2 tile shape: 32 x 8*ty voxel columns (ty = 1 or 4, default 1) by kz
  * z-slices (1..64, default 4).  Results are bit-identical for every shape. */
 int psfs_set_voxel_tile(psfs_handle *h, int32_t ty, int32_t kz);

@@ -77,6 +77,7 @@ struct VParams {
     int32_t ntiles;
     int32_t ty;                        // y sub-tiles per warp (1 or 4): tile = 32 x 8ty columns
     int32_t kz;                        // z-slices per tile
+    int32_t max_blocks_per_sm;         // 0: fill the SMs (occupancy); > 0: cap (overlap)
 };
 
 // Launchers (psfs_kernels.cu).  Return the cudaError_t of the launch.
