@@ -404,6 +404,58 @@ def run_ours(args):
                "how": "psfs_reconstruct_host: pinned host frames -> device staging (copy stream), "
                       "both stages, bitmask -> pinned host (second copy stream), double-buffered"}
 
+    # ---- secondary: the two kernels in isolation (serial schedule), so their
+    # roofline fractions are not diluted by the overlap of the headline schedule
+    isolated = None
+    if not args.profile and args.overlap >= 0:
+        rec.set_overlap(False)
+        rec.set_profiling(True)
+        rec.kernel_times(reset=True)
+        for k in range(min(args.steps, 10)):
+            flush.fill_(k)
+            flush_sum = flush_rd.sum()
+            step(args.warmup + k)
+        torch.cuda.synchronize(dev)
+        kti = rec.kernel_times(reset=True)
+        rec.set_profiling(False)
+        rec.set_overlap(True, max(args.overlap, 0))
+        isolated = {}
+        for name, (ms_, n_) in kti.items():
+            avg = (ms_ / max(n_, 1)) / 1e3
+            ab = s1_bytes if name == "k_likelihood" else s2_bytes
+            pk = per_kernel[name]["peak"]
+            isolated[name] = {"avg_launch_us": avg * 1e6, "achieved": ab / avg / 1e9,
+                              "frac": ab / avg / 1e9 / pk}
+        roofline["isolated_serial"] = isolated
+
+    # ---- secondary: bits-only early exit (psfs_set_carve), identical bitmask;
+    # reported beside the headline, never as it
+    carve = None
+    if not args.profile:
+        rec.set_carve(True)
+        for k in range(args.warmup):
+            step(k)
+        torch.cuda.synchronize(dev)
+        cms = 0.0
+        for k in range(args.steps):
+            flush.fill_(k)
+            flush_sum = flush_rd.sum()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step(args.warmup + k)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            cms += e0.elapsed_time(e1)
+        rec.set_carve(False)
+        if world > 1:
+            t = torch.tensor([cms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            cms = float(t.item())
+        carve = {"value": world * B * args.steps / (cms / 1e3), "unit": "frames/s",
+                 "ms_per_step": cms / args.steps,
+                 "note": "bits-only early exit (psfs_set_carve): a warp stops adding cameras once "
+                         "its voxels are provably unoccupied; bitmask identical; not the headline"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         nthreads = host_cores()
@@ -428,7 +480,7 @@ def run_ours(args):
                                     + (f" (k_voxel capped at {args.overlap} blocks/SM)" if args.overlap > 0 else "")
                                     if args.overlap >= 0 else "serial"),
                        "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the step events)"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "carve": carve,
             "gpu_launches": launches, "clocks": clocks,
             "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms),
                         "max": max(step_ms)},

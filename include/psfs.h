@@ -188,6 +188,13 @@ int psfs_set_roi_enabled(psfs_handle *h, int32_t enabled);
  * (DESIGN.md §8 has the measurements that made 0 the default). */
 int psfs_set_stage1_path(psfs_handle *h, int32_t path);
 
+/* Bits-only early exit (default off): when a call requests no log-odds, a
+ * warp stops adding cameras once every one of its voxels and frames satisfies
+ * S + (cameras left) * q_max <= T_q, q_max = rint(-ln p_O 2^20) + 1 bounding
+ * every term -- the occupancy bit is then provably 0 and the bitmask is
+ * identical to the full sum's.  Ignored when log-odds are requested. */
+int psfs_set_carve(psfs_handle *h, int32_t enabled);
+
 /* Overlapped batches (default on): with more than one frame group in a
  * psfs_reconstruct_batch call, stage 1 of group g+1 runs on an internal stream
  * beside stage 2 of group g (two term buffers); voxel_blocks_per_sm > 0 caps

@@ -78,6 +78,8 @@ struct VParams {
     int32_t ty;                        // y sub-tiles per warp (1 or 4): tile = 32 x 8ty columns
     int32_t kz;                        // z-slices per tile
     int32_t max_blocks_per_sm;         // 0: fill the SMs (occupancy); > 0: cap (overlap)
+    int32_t carve;                     // bits-only early exit (no log-odds output)
+    int32_t q_max;                     // largest possible term: rint(-ln p_O 2^20)
 };
 
 // Launchers (psfs_kernels.cu).  Return the cudaError_t of the launch.

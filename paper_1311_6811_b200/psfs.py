@@ -33,7 +33,8 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_debug_terms", "psfs_debug_roi", "psfs_set_roi_enabled", "psfs_set_max_fuse",
            "psfs_last_launch_count", "psfs_set_profiling", "psfs_kernel_times",
            "psfs_fast_rcp_enabled", "psfs_debug_rcp_check", "psfs_probe_l1_bandwidth",
-           "psfs_set_stage1_path", "psfs_set_voxel_tile", "psfs_set_overlap"]
+           "psfs_set_stage1_path", "psfs_set_voxel_tile", "psfs_set_overlap",
+           "psfs_set_carve"]
 
 
 class PsfsError(RuntimeError):
@@ -91,6 +92,7 @@ def lib():
         L.psfs_set_stage1_path.argtypes = [vp, i32]
         L.psfs_set_voxel_tile.argtypes = [vp, i32, i32]
         L.psfs_set_overlap.argtypes = [vp, i32, i32]
+        L.psfs_set_carve.argtypes = [vp, i32]
         L.psfs_last_launch_count.argtypes = [vp]
         L.psfs_set_profiling.argtypes = [vp, i32]
         L.psfs_kernel_times.argtypes = [vp, vp, vp, i32]
@@ -213,6 +215,10 @@ class Reconstructor:
 
     def set_max_fuse(self, fmax: int):
         self._check(lib().psfs_set_max_fuse(self._h, int(fmax)), "psfs_set_max_fuse")
+
+    def set_carve(self, on: bool):
+        """Bits-only early exit (exact bitmask; ignored when log-odds are requested)."""
+        self._check(lib().psfs_set_carve(self._h, int(bool(on))), "psfs_set_carve")
 
     def set_overlap(self, on: bool, voxel_blocks_per_sm: int = 0):
         self._check(lib().psfs_set_overlap(self._h, int(bool(on)), int(voxel_blocks_per_sm)),

@@ -120,3 +120,29 @@ def test_overlapped_batches_bit_identical():
         b.reconstruct_batch(fr, 21, logodds=Lb, bits=Bb)
     torch.cuda.synchronize()
     assert torch.equal(Ba, Bb) and torch.equal(La, Lb)
+
+
+@pytest.mark.parametrize("params", [dict(), dict(occlusion_prior=0.3, voxel_prior=0.2, threshold=0.7)])
+def test_carve_bits_identical(params):
+    """psfs_set_carve: the bits-only early exit leaves the bitmask unchanged
+    (C2 skeleton frames and C1 with general priors), and is ignored when
+    log-odds are requested."""
+    from paper_1311_6811_b200 import from_scene
+    name = "C2" if not params else "C1"
+    s = make_scene(name)
+    frames = np.stack([make_frames(s, f) for f in range(8)])
+    fr = torch.from_numpy(frames).cuda()
+    a = from_scene(s, params)
+    b = from_scene(s, params)
+    b.set_carve(True)
+    _, Ba = a.alloc_outputs(8, logodds=False)
+    _, Bb = b.alloc_outputs(8, logodds=False)
+    a.reconstruct_batch(fr, 8, bits=Ba)
+    b.reconstruct_batch(fr, 8, bits=Bb)
+    Lc, Bc = b.alloc_outputs(8)
+    b.reconstruct_batch(fr, 8, logodds=Lc, bits=Bc)
+    La, Bd = a.alloc_outputs(8)
+    a.reconstruct_batch(fr, 8, logodds=La, bits=Bd)
+    torch.cuda.synchronize()
+    assert torch.equal(Ba, Bb)
+    assert torch.equal(Bc, Bd) and torch.equal(Lc, La)
