@@ -83,7 +83,7 @@ def test_fixed_point_headroom_rejected():
     from paper_1311_6811_b200 import Reconstructor
     from paper_1311_6811_b200.psfs import PsfsError
     s = make_scene("C1")
-    r = Reconstructor(s.grid, params=dict(sigma_floor=1e-30))
+    r = Reconstructor(s.grid, params=dict(sigma_floor=1e-100))
     with pytest.raises(PsfsError) as e:
         r.set_cameras(s.P, s.widths, s.heights)
     assert e.value.code == 1
