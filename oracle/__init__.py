@@ -66,6 +66,8 @@ def lib():
         _lib.oracle_projection_flips.argtypes = [C.POINTER(_Rig), vp, C.POINTER(_Grid), i, i, i]
         _lib.oracle_projection_flips.restype = i64
         _lib.oracle_max_threads.restype = i
+        _lib.oracle_surface.argtypes = [vp, C.POINTER(_Grid), i, i, vp, i64]
+        _lib.oracle_surface.restype = i64
     return _lib
 
 
@@ -233,6 +235,19 @@ def projection_flips(P, W, H, grid, k0=0, k1=None, p_occ=0.5, nthreads=1) -> int
     g = _grid(grid)
     return int(lib().oracle_projection_flips(C.byref(rh.rig), _p(P), C.byref(g), int(k0),
                                              int(k1), int(nthreads)))
+
+
+def surface(bits, grid, k0=0, k1=None):
+    """NEXT-2: linear indices (ascending) of the
+    occupied voxels of slices [k0,k1) with at least one unoccupied 6-neighbour;
+    outside the volume counts as unoccupied.  bits: uint32 words of the full grid."""
+    k1 = grid.zlen if k1 is None else k1
+    b = np.ascontiguousarray(np.asarray(bits).view(np.uint32))
+    g = _grid(grid)
+    n = int(lib().oracle_surface(_p(b), C.byref(g), int(k0), int(k1), None, 0))
+    out = np.empty(max(n, 1), np.int64)
+    lib().oracle_surface(_p(b), C.byref(g), int(k0), int(k1), _p(out), n)
+    return out[:n]
 
 
 def scene_reconstruct(scene, frames, **kw):

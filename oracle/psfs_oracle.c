@@ -325,6 +325,40 @@ void oracle_project_pinned_batch(const float A[12], int W, int H, int64_t n, con
     }
 }
 
+/* ------------------------------------------------------------------------ */
+/* NEXT-2: inner-voxel removal ("remove voxels inside human body and   */
+/* get the surface voxels", "Remove inner voxel").           */
+/* ------------------------------------------------------------------------ */
+
+static int occupied(const uint32_t *bits, const oracle_grid *g, int i, int j, int k)
+{
+    /* outside the volume counts as unoccupied */
+    if (i < 0 || j < 0 || k < 0 || i >= g->xlen || j >= g->ylen || k >= g->zlen) return 0;
+    const int64_t v = (int64_t)i + (int64_t)g->xlen * (j + (int64_t)g->ylen * k);
+    return (int)((bits[v >> 5] >> (v & 31)) & 1u);
+}
+
+/* Surface voxels of slices [k0,k1): occupied voxels with at least one
+ * unoccupied 6-neighbour.  Writes their linear indices in increasing order
+ * (up to `capacity`) and returns how many there are. */
+int64_t oracle_surface(const uint32_t *bits, const oracle_grid *g, int k0, int k1,
+                       int64_t *out, int64_t capacity)
+{
+    int64_t n = 0;
+    for (int k = k0; k < k1; ++k)
+        for (int j = 0; j < g->ylen; ++j)
+            for (int i = 0; i < g->xlen; ++i) {
+                if (!occupied(bits, g, i, j, k)) continue;
+                const int inner = occupied(bits, g, i - 1, j, k) && occupied(bits, g, i + 1, j, k) &&
+                                  occupied(bits, g, i, j - 1, k) && occupied(bits, g, i, j + 1, k) &&
+                                  occupied(bits, g, i, j, k - 1) && occupied(bits, g, i, j, k + 1);
+                if (inner) continue;
+                if (n < capacity) out[n] = (int64_t)i + (int64_t)g->xlen * (j + (int64_t)g->ylen * k);
+                ++n;
+            }
+    return n;
+}
+
 int oracle_max_threads(void)
 {
 #ifdef _OPENMP

@@ -39,6 +39,8 @@ int64_t oracle_projection_flips(const oracle_rig *rig, const double *P, const or
                                 int k0, int k1, int nthreads);
 void oracle_project_pinned_batch(const float A[12], int W, int H, int64_t n, const int32_t *ijk,
                                   int32_t *out);
+int64_t oracle_surface(const uint32_t *bits, const oracle_grid *g, int k0, int k1, int64_t *out,
+                       int64_t capacity);
 int oracle_max_threads(void);
 
 #endif
