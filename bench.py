@@ -456,6 +456,27 @@ def run_ours(args):
                  "note": "bits-only early exit (psfs_set_carve): a warp stops adding cameras once "
                          "its voxels are provably unoccupied; bitmask identical; not the headline"}
 
+    # ---- secondary: NEXT-2 surface extraction (psfs_surface) of one frame's bitmask
+    surface = None
+    if not args.profile:
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        idx = torch.empty(nvox, dtype=torch.int64, device=dev)
+        sbits = torch.empty_like(Bits[0])
+        for _ in range(3):
+            rec.surface(Bits[0], surface_bits=sbits, indices=idx, count=cnt, stream=stream)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(20):
+            rec.surface(Bits[0], surface_bits=sbits, indices=idx, count=cnt, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        surface = {"us_per_frame": e0.elapsed_time(e1) / 20 * 1e3, "surface_voxels": int(cnt.item()),
+                   "occupied_voxels": int(torch.bitwise_and(
+                       Bits[0].view(-1, 1) >> torch.arange(32, device=dev, dtype=torch.int32), 1).sum().item()),
+                   "note": "NEXT-2 inner-voxel removal (P:301): bit-parallel 6-neighbour test + ordered "
+                           "compaction, 3 launches, not part of the headline step"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         nthreads = host_cores()
@@ -481,6 +502,7 @@ def run_ours(args):
                                     if args.overlap >= 0 else "serial"),
                        "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the step events)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "carve": carve,
+            "surface": surface,
             "gpu_launches": launches, "clocks": clocks,
             "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms),
                         "max": max(step_ms)},

@@ -153,6 +153,19 @@ int psfs_reconstruct_batch(psfs_handle *h, int32_t nframes, const uint8_t *const
 int psfs_reconstruct_host(psfs_handle *h, int32_t nframes, const uint8_t *const *frames,
                           float *logodds, uint32_t *bits, void *cuda_stream);
 
+/* NEXT-2, inner-voxel removal ("remove voxels inside human body and get
+ * the surface voxels"): the occupied voxels of this handle's
+ * slab with at least one unoccupied 6-neighbour, voxels outside the volume
+ * counting as unoccupied.  bits: DEVICE, the FULL grid's words (after the
+ * all-gather in a z-slab partition).  surface_bits: DEVICE, nullable, full-grid
+ * words; the slab's words are written.  indices: DEVICE, nullable, up to
+ * `capacity` int64 linear voxel indices in increasing order.  count: DEVICE,
+ * one int64, the exact number of surface voxels of the slab (also when it
+ * exceeds capacity).  Asynchronous on cuda_stream.
+ * Errors: PSFS_EINVAL, PSFS_ENOMEM, PSFS_ECUDA. */
+int psfs_surface(psfs_handle *h, const uint32_t *bits, uint32_t *surface_bits, int64_t *indices,
+                 int64_t capacity, int64_t *count, void *cuda_stream);
+
 void psfs_destroy(psfs_handle *h);
 
 const char *psfs_status_string(int status);

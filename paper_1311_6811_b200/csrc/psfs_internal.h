@@ -87,6 +87,10 @@ cudaError_t launch_likelihood(const S1Params &p, int F, int max_roi_px, int path
 cudaError_t launch_prep_model(ModelPx *model, int64_t begin, int64_t n, double c0, cudaStream_t s);
 cudaError_t launch_voxel(const VParams &p, int F, cudaStream_t s, int *nblocks);
 int voxel_tiles(int xlen, int ylen, int k0, int k1, int ty, int kz);
+cudaError_t launch_surface(const uint32_t *bits, uint32_t *surf, int64_t *idx, int64_t capacity,
+                           int64_t *count, long long *block_scratch, int xlen, int ylen, int zlen,
+                           int k0, int k1, cudaStream_t s, int *launches);
+int surface_blocks(int xlen, int ylen, int k0, int k1);
 cudaError_t launch_l1_probe(const void *buf, int blocks, int iters, int *out, cudaStream_t s);
 cudaError_t launch_rcp_check(uint32_t lo_bits, uint32_t hi_bits, unsigned long long *bad,
                              cudaStream_t s);

@@ -34,7 +34,7 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_last_launch_count", "psfs_set_profiling", "psfs_kernel_times",
            "psfs_fast_rcp_enabled", "psfs_debug_rcp_check", "psfs_probe_l1_bandwidth",
            "psfs_set_stage1_path", "psfs_set_voxel_tile", "psfs_set_overlap",
-           "psfs_set_carve"]
+           "psfs_set_carve", "psfs_surface"]
 
 
 class PsfsError(RuntimeError):
@@ -93,6 +93,7 @@ def lib():
         L.psfs_set_voxel_tile.argtypes = [vp, i32, i32]
         L.psfs_set_overlap.argtypes = [vp, i32, i32]
         L.psfs_set_carve.argtypes = [vp, i32]
+        L.psfs_surface.argtypes = [vp, vp, vp, vp, C.c_int64, vp, vp]
         L.psfs_last_launch_count.argtypes = [vp]
         L.psfs_set_profiling.argtypes = [vp, i32]
         L.psfs_kernel_times.argtypes = [vp, vp, vp, i32]
@@ -320,6 +321,22 @@ class Reconstructor:
         s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
         self._check(lib().psfs_reconstruct_host(self._h, int(nframes), ptrs, hp(logodds_host),
                                                 hp(bits_host), s), "psfs_reconstruct_host")
+
+    def surface(self, bits, surface_bits=None, indices=None, count=None, stream=None):
+        """Surface voxels (NEXT-2) of this handle's slab from a full-grid bitmask
+        (int32 CUDA tensor of nwords).  Returns (count tensor [1] int64, indices
+        tensor or None, surface_bits or None); everything stays on the device."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        if count is None:
+            count = torch.zeros(1, dtype=torch.int64, device=dev)
+        cap = 0 if indices is None else indices.numel()
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._check(lib().psfs_surface(self._h, _dev_ptr(bits, torch.int32),
+                                       _dev_ptr(surface_bits, torch.int32),
+                                       _dev_ptr(indices, torch.int64), cap,
+                                       _dev_ptr(count, torch.int64), s), "psfs_surface")
+        return count, indices, surface_bits
 
     # -- introspection ----------------------------------------------------------
     def debug_terms(self, frames, stream=None):
