@@ -68,6 +68,7 @@ def lib():
         _lib.oracle_max_threads.restype = i
         _lib.oracle_surface.argtypes = [vp, C.POINTER(_Grid), i, i, vp, i64]
         _lib.oracle_surface.restype = i64
+        _lib.oracle_smooth_threshold.argtypes = [vp, C.POINTER(_Grid), d, vp, vp]
     return _lib
 
 
@@ -248,6 +249,18 @@ def surface(bits, grid, k0=0, k1=None):
     out = np.empty(max(n, 1), np.int64)
     lib().oracle_surface(_p(b), C.byref(g), int(k0), int(k1), _p(out), n)
     return out[:n]
+
+
+def smooth_threshold(post, grid, tau=0.5):
+    """NEXT-1: 3x3x3 zero-padded box average
+    of the posterior (float64 [nvox], x-fastest), then occupied := smoothed > tau.
+    Returns (smoothed float64 [nvox], bits uint32 words)."""
+    post = np.ascontiguousarray(np.asarray(post, np.float64).reshape(-1))
+    g = _grid(grid)
+    sm = np.empty_like(post)
+    bits = np.zeros((post.size + 31) // 32, np.uint32)
+    lib().oracle_smooth_threshold(_p(post), C.byref(g), float(tau), _p(sm), _p(bits))
+    return sm, bits
 
 
 def scene_reconstruct(scene, frames, **kw):

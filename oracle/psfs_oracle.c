@@ -359,6 +359,35 @@ int64_t oracle_surface(const uint32_t *bits, const oracle_grid *g, int k0, int k
     return n;
 }
 
+/* ------------------------------------------------------------------------ */
+/* NEXT-1: probability filtering + thresholding, merged ("we filter the */
+/* probability of voxels ... and then perform a thresholding process";        */
+/* P:269-271): 3x3x3 box average of the posterior with zero */
+/* padding outside the volume, then occupied := smoothed > tau.               */
+/* ------------------------------------------------------------------------ */
+void oracle_smooth_threshold(const double *post, const oracle_grid *g, double tau, double *smoothed,
+                             uint32_t *bits_out)
+{
+    /* bits_out (if given) must be zeroed by the caller */
+    for (int k = 0; k < g->zlen; ++k)
+        for (int j = 0; j < g->ylen; ++j)
+            for (int i = 0; i < g->xlen; ++i) {
+                double acc = 0.0;
+                for (int dk = -1; dk <= 1; ++dk)
+                    for (int dj = -1; dj <= 1; ++dj)
+                        for (int di = -1; di <= 1; ++di) {
+                            const int a = i + di, b = j + dj, c = k + dk;
+                            if (a < 0 || b < 0 || c < 0 || a >= g->xlen || b >= g->ylen || c >= g->zlen)
+                                continue; /* zero padding */
+                            acc += post[(int64_t)a + (int64_t)g->xlen * (b + (int64_t)g->ylen * c)];
+                        }
+                const double sm = acc / 27.0;
+                const int64_t v = (int64_t)i + (int64_t)g->xlen * (j + (int64_t)g->ylen * k);
+                if (smoothed) smoothed[v] = sm;
+                if (bits_out && sm > tau) bits_out[v >> 5] |= 1u << (v & 31);
+            }
+}
+
 int oracle_max_threads(void)
 {
 #ifdef _OPENMP

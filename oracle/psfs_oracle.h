@@ -41,6 +41,8 @@ void oracle_project_pinned_batch(const float A[12], int W, int H, int64_t n, con
                                   int32_t *out);
 int64_t oracle_surface(const uint32_t *bits, const oracle_grid *g, int k0, int k1, int64_t *out,
                        int64_t capacity);
+void oracle_smooth_threshold(const double *post, const oracle_grid *g, double tau, double *smoothed,
+                             uint32_t *bits_out);
 int oracle_max_threads(void);
 
 #endif
