@@ -477,6 +477,26 @@ def run_ours(args):
                    "note": "NEXT-2 inner-voxel removal (P:301): bit-parallel 6-neighbour test + ordered "
                            "compaction, 3 launches, not part of the headline step"}
 
+    # ---- secondary: NEXT-1 merged filtering + thresholding (psfs_smooth_threshold)
+    smooth = None
+    if not args.profile:
+        Lf, Bf = rec.alloc_outputs(1)
+        rec.reconstruct(frames_dev[0], logodds=Lf, bits=Bf, stream=stream)
+        smv = torch.empty_like(Lf[0])
+        smb = torch.empty_like(Bf[0])
+        for _ in range(3):
+            rec.smooth_threshold(Lf[0], smoothed=smv, bits=smb, stream=stream)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(20):
+            rec.smooth_threshold(Lf[0], smoothed=smv, bits=smb, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        smooth = {"us_per_frame": e0.elapsed_time(e1) / 20 * 1e3,
+                  "note": "NEXT-1 posterior 3x3x3 box filter + threshold (P:111, P:300), "
+                          "2 launches, not part of the headline step"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         nthreads = host_cores()
@@ -502,7 +522,7 @@ def run_ours(args):
                                     if args.overlap >= 0 else "serial"),
                        "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the step events)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "carve": carve,
-            "surface": surface,
+            "surface": surface, "smooth": smooth,
             "gpu_launches": launches, "clocks": clocks,
             "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms),
                         "max": max(step_ms)},

@@ -166,6 +166,18 @@ int psfs_reconstruct_host(psfs_handle *h, int32_t nframes, const uint8_t *const 
 int psfs_surface(psfs_handle *h, const uint32_t *bits, uint32_t *surface_bits, int64_t *indices,
                  int64_t capacity, int64_t *count, void *cuda_stream);
 
+/* NEXT-1, probability filtering + thresholding merged ("we filter the
+ * probability of voxels ... and then perform a thresholding process";
+ * P:269-271): posterior P = 1/(1 + e^-L) from the log-odds,
+ * 3x3x3 box average with zero padding outside the volume, occupied :=
+ * smoothed > tau (the handle's threshold).  logodds: DEVICE, the whole grid
+ * (x-fastest floats, e.g. psfs_reconstruct's output); smoothed: DEVICE,
+ * nullable, nvox floats; bits: DEVICE, nullable, full-grid words.  World-1
+ * handles only (a z-slab would need a one-slice halo from its neighbours).
+ * Errors: PSFS_EINVAL, PSFS_ENOMEM, PSFS_ECUDA. */
+int psfs_smooth_threshold(psfs_handle *h, const float *logodds, float *smoothed, uint32_t *bits,
+                          void *cuda_stream);
+
 void psfs_destroy(psfs_handle *h);
 
 const char *psfs_status_string(int status);

@@ -91,6 +91,8 @@ cudaError_t launch_surface(const uint32_t *bits, uint32_t *surf, int64_t *idx, i
                            int64_t *count, long long *block_scratch, int xlen, int ylen, int zlen,
                            int k0, int k1, cudaStream_t s, int *launches);
 int surface_blocks(int xlen, int ylen, int k0, int k1);
+cudaError_t launch_smooth(const float *logodds, float *P, float *smoothed, uint32_t *bits, int xlen,
+                          int ylen, int zlen, float tau, cudaStream_t s);
 cudaError_t launch_l1_probe(const void *buf, int blocks, int iters, int *out, cudaStream_t s);
 cudaError_t launch_rcp_check(uint32_t lo_bits, uint32_t hi_bits, unsigned long long *bad,
                              cudaStream_t s);

@@ -34,7 +34,7 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_last_launch_count", "psfs_set_profiling", "psfs_kernel_times",
            "psfs_fast_rcp_enabled", "psfs_debug_rcp_check", "psfs_probe_l1_bandwidth",
            "psfs_set_stage1_path", "psfs_set_voxel_tile", "psfs_set_overlap",
-           "psfs_set_carve", "psfs_surface"]
+           "psfs_set_carve", "psfs_surface", "psfs_smooth_threshold"]
 
 
 class PsfsError(RuntimeError):
@@ -94,6 +94,7 @@ def lib():
         L.psfs_set_overlap.argtypes = [vp, i32, i32]
         L.psfs_set_carve.argtypes = [vp, i32]
         L.psfs_surface.argtypes = [vp, vp, vp, vp, C.c_int64, vp, vp]
+        L.psfs_smooth_threshold.argtypes = [vp, vp, vp, vp, vp]
         L.psfs_last_launch_count.argtypes = [vp]
         L.psfs_set_profiling.argtypes = [vp, i32]
         L.psfs_kernel_times.argtypes = [vp, vp, vp, i32]
@@ -337,6 +338,17 @@ class Reconstructor:
                                        _dev_ptr(indices, torch.int64), cap,
                                        _dev_ptr(count, torch.int64), s), "psfs_surface")
         return count, indices, surface_bits
+
+    def smooth_threshold(self, logodds, smoothed=None, bits=None, stream=None):
+        """NEXT-1: box-filtered posterior and its threshold bits from a full-grid
+        log-odds tensor (float32 CUDA, nvox).  Outputs are caller-owned tensors."""
+        import torch
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._check(lib().psfs_smooth_threshold(self._h, _dev_ptr(logodds, torch.float32),
+                                                _dev_ptr(smoothed, torch.float32),
+                                                _dev_ptr(bits, torch.int32), s),
+                    "psfs_smooth_threshold")
+        return smoothed, bits
 
     # -- introspection ----------------------------------------------------------
     def debug_terms(self, frames, stream=None):
