@@ -45,11 +45,11 @@ def parse():
     ap.add_argument("--overlap", type=int, default=0,
                     help="overlap stage 1 of group g+1 with stage 2 of group g; value = k_voxel "
                          "blocks/SM cap (0: none); -1: serial schedule")
-    ap.add_argument("--fuse", type=int, default=8, help="frames fused per kernel pass")
+    ap.add_argument("--fuse", type=int, default=16, help="frames fused per kernel pass")
     ap.add_argument("--config", default="C2")
     ap.add_argument("--ty", type=int, default=1)
     ap.add_argument("--kz", type=int, default=4)
-    ap.add_argument("--stage1", type=int, default=0, choices=[0, 1, 2, 3, 4],
+    ap.add_argument("--stage1", type=int, default=0, choices=[0, 1, 2, 3, 4, 5],
                     help="stage-1 kernel: 0 one pixel/thread, 1 TMA ring, 2 pipelined, "
                          "3 four pixels/thread, 4 warp-row loads (A/B experiments)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -133,11 +133,18 @@ def make_workload(config, n_distinct, seed_offset=0):
 
 
 def gather_sectors(scene, F):
-    """Algorithmic L1 sector count of one k_voxel launch: for every warp (8 x 4
-    voxels in x, y at one z), camera and slice, the number of distinct pixels the
-    32 voxel centres project to (each pixel's F terms are one 32-byte sector for
-    F = 8).  Nearest pixel in double precision (the pinned FP32 pixel differs on
-    ~0.1 % of voxel-cameras, irrelevant for a count)."""
+    """Algorithmic L1 wavefront count of one k_voxel launch.  The L1TEX data pipe
+    serves about one 128-byte line per clock whatever number of its sectors a
+    request touches (scripts/micro/gather.cu), so the unit is the line:
+    * F <= 8 (k_voxel): for every warp (8 x 4 voxels in x, y at one z), camera
+      and slice, the distinct pixels its 32 voxel centres project to (a pixel's
+      F terms are one sector of one line);
+    * F = 16 (k_voxel16, lane pairs): two gathers per warp and camera, over the
+      16 even and the 16 odd voxels of the tile; a pixel's 64-byte record is two
+      sectors of one line.
+    Nearest pixel in double precision (the pinned FP32 pixel differs on ~0.1 %
+    of voxel-cameras, irrelevant for a count).  Returns (wavefronts, useful bytes
+    per wavefront)."""
     g = scene.grid
     i = np.arange(g.xlen)
     j = np.arange(g.ylen)
@@ -157,10 +164,11 @@ def gather_sectors(scene, F):
             pix = np.where(inview, v * (scene.widths[c] + 1) + u, -1)   # -1: the zero pad
             # [ylen, xlen] -> warps of 4 rows x 8 columns
             t = pix.reshape(g.ylen // 4, 4, g.xlen // 8, 8).transpose(0, 2, 1, 3).reshape(-1, 32)
-            t = np.sort(t, axis=1)
-            total += int((1 + (np.diff(t, axis=1) != 0).sum(axis=1)).sum())
-    sector_bytes = 32 if F == 8 else 4 * F
-    return total, total * sector_bytes
+            groups = [t] if F <= 8 else [t[:, 0::2], t[:, 1::2]]
+            for tt in groups:
+                tt = np.sort(tt, axis=1)
+                total += int((1 + (np.diff(tt, axis=1) != 0).sum(axis=1)).sum())
+    return total, 4 * F
 
 
 def cpu_baseline(scene, frames, seconds, nthreads):
@@ -339,16 +347,18 @@ def run_ours(args):
     # the planned pixel rectangle
     s1_bytes = roi_px * (24 + 7 * F)
     s1_avg_s = (l_ms / max(l_n, 1)) / 1e3
-    # stage 2: the gather is bound by the L1TEX data pipe, one 32-byte sector per
-    # clock per SM for 32-byte-per-lane loads (ncu: l1tex__data_pipe_lsu_wavefronts
-    # equals the sectors requested); algorithmic sectors = distinct pixels per
-    # warp-gather for this tiling (gather_sectors), peak = 1 sector/clk/SM
+    # stage 2: the gather is bound by the L1TEX data pipe, one line-wavefront per
+    # clock per SM (ncu: l1tex__data_pipe_lsu_wavefronts); algorithmic wavefronts =
+    # distinct pixels per warp-gather for this tiling (gather_sectors), each
+    # carrying wf_bytes useful bytes (32: one sector, F = 8; 64: two sectors of
+    # one line, F = 16); peak = 1 wavefront/clk/SM x wf_bytes
     v_avg_s = (v_ms / max(v_n, 1)) / 1e3
-    sectors, s2_bytes = gather_sectors(scene, F)
+    sectors, wf_bytes = gather_sectors(scene, F)
+    s2_bytes = sectors * wf_bytes
     sm_clk = (clocks or {}).get("sm_mhz") or float(peaks.get("sm_max_mhz", 1965.0))
     import torch as _t
     nsm = _t.cuda.get_device_properties(dev).multi_processor_count
-    l1_sector_peak = nsm * sm_clk * 1e6 * 32 / 1e9
+    l1_sector_peak = nsm * sm_clk * 1e6 * wf_bytes / 1e9
     per_kernel = {
         "k_likelihood": {
             "bound": "hbm", "achieved": s1_bytes / s1_avg_s / 1e9, "peak": hbm_peak,
@@ -357,10 +367,10 @@ def run_ours(args):
         "k_voxel": {
             "bound": "l1", "achieved": s2_bytes / v_avg_s / 1e9, "peak": l1_sector_peak,
             "unit": "GB/s",
-            "peak_source": f"derived: {nsm} SMs x 1 L1TEX data-pipe wavefront/clk x 32-byte "
-                           f"sector x {sm_clk:.0f} MHz (median SM clock of this run); "
-                           "DESIGN.md section 8",
-            "algorithmic_bytes_per_launch": s2_bytes, "sectors_per_launch": sectors,
+            "peak_source": f"derived: {nsm} SMs x 1 L1TEX data-pipe wavefront/clk x {wf_bytes} "
+                           f"useful bytes per wavefront x {sm_clk:.0f} MHz (median SM clock of "
+                           "this run); DESIGN.md section 8",
+            "algorithmic_bytes_per_launch": s2_bytes, "wavefronts_per_launch": sectors,
             "avg_launch_us": v_avg_s * 1e6,
             "voxel_cam_frames_per_s": nvox * ncam * F / v_avg_s, "traffic": traffic.get("k_voxel"),
             "l1_load_probe_gbs": l1_peak},

@@ -62,7 +62,7 @@ enum {
 };
 
 #define PSFS_MAX_CAMERAS 64 /* per handle                                  */
-#define PSFS_MAX_BATCH 8    /* frames fused into one stage-1/stage-2 pass  */
+#define PSFS_MAX_BATCH 16   /* frames fused into one stage-1/stage-2 pass  */
 
 typedef struct psfs_handle psfs_handle; /* opaque, library-owned */
 
@@ -231,7 +231,9 @@ int psfs_set_overlap(psfs_handle *h, int32_t enabled, int32_t voxel_blocks_per_s
  * z-slices (1..64, default 4).  Results are bit-identical for every shape. */
 int psfs_set_voxel_tile(psfs_handle *h, int32_t ty, int32_t kz);
 
-/* Cap the number of frames fused into one pass (1, 2, 4 or 8; default 8). */
+/* Cap the number of frames fused into one pass (1, 2, 4, 8 or 16; default 16).
+ * A 16-frame pass stores 64-byte term records (two sectors of one 128-byte
+ * line) that two lanes of k_voxel read together. */
 int psfs_set_max_fuse(psfs_handle *h, int32_t fmax);
 
 /* Per-kernel device timing (bench instrumentation): when enabled, every

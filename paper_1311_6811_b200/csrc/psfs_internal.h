@@ -7,7 +7,7 @@
 namespace psfs {
 
 constexpr int kMaxCam = 64;  // == PSFS_MAX_CAMERAS
-constexpr int kMaxF = 8;     // == PSFS_MAX_BATCH
+constexpr int kMaxF = 16;    // == PSFS_MAX_BATCH
 constexpr int kQBits = 20;   // Q11.20 fixed point for the per-view term t
 
 // Background model of one pixel as stored on the device (set once by
@@ -31,7 +31,9 @@ struct S1Cam {
     int32_t seg_begin;       // TMA path: first segment index of this camera
     int32_t segs_per_row;    // TMA path: ceil((c1 - c0) / kSeg)
     int32_t q_begin;         // pipelined path: first ROI pixel index of this camera
-    int32_t pad_;
+    int32_t ch_begin;        // async path: first 32-pixel row chunk of this camera
+    int32_t ch_per_row;      // async path: ceil((c1 - c0) / 32)
+    int32_t pad_[3];
 };
 
 constexpr int kSeg = 512;  // pixels per TMA segment (one row chunk) = consumer threads per block
@@ -40,7 +42,7 @@ struct S1Params {
     S1Cam cam[kMaxCam];
     const uint8_t *frames[kMaxF][kMaxCam];  // [f][c] device pointers, H*W*3 RGB
     const struct ModelPx *model;            // total_px records (AoS, 32 B each)
-    int32_t *terms;                         // (off + p) * F + f, 32-B aligned
+    int32_t *terms;                         // (toff + p) * tf + f, 32-B aligned
     int64_t total_px;
     double ln_po;    // ln p_O
     double ln_1mpo;  // ln (1 - p_O)
@@ -48,6 +50,9 @@ struct S1Params {
     int32_t ncam;
     int32_t nseg;    // TMA path: total segments over all cameras
     int32_t nq;      // pipelined path: total ROI pixels over all cameras
+    int32_t nchunk;  // async path: 32-pixel row chunks over all cameras
+    int32_t tf;      // frames per term record (the pass's F: 1..16)
+    int32_t halves;  // 2: a 16-frame pass run as two 8-frame halves (path 0/4 only)
 };
 
 // Stage 2 (voxel) launch description.

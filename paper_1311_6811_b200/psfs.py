@@ -24,7 +24,7 @@ PSFS_OK = 0
 STATUS = {0: "PSFS_OK", 1: "PSFS_EINVAL", 2: "PSFS_EDEGENERATE", 3: "PSFS_EDIM", 4: "PSFS_ECOUNT",
           5: "PSFS_ESTATE", 6: "PSFS_ECUDA", 7: "PSFS_ENOMEM", 8: "PSFS_ELIMIT"}
 MAX_CAMERAS = 64
-MAX_BATCH = 8
+MAX_BATCH = 16
 
 # Every symbol include/psfs.h declares (checked by tests/test_abi.py).
 EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_background",

@@ -52,7 +52,7 @@ def test_camera_inside_grid_uses_exact_reciprocal_and_matches_oracle():
     assert_parity(g["L"][0], g["bits"][0], orc, s.grid.nvox)
 
 
-@pytest.mark.parametrize("path", [0, 2, 3, 4])
+@pytest.mark.parametrize("path", [0, 2, 3, 4, 5])
 def test_stage1_paths_bit_identical(path):
     """The three stage-1 kernels (TMA ring with cp.async.bulk + mbarrier, used
     when frames are 16-byte aligned and W % 16 == 0; pipelined persistent; one
@@ -83,6 +83,30 @@ def test_stage1_paths_bit_identical(path):
         assert torch.equal(r.debug_terms(aligned[0]), ref.debug_terms(shifted[0]))
 
 
+@pytest.mark.parametrize("path,ty,kz", [(0, 1, 1), (4, 1, 4), (0, 1, 16), (0, 4, 1), (4, 4, 3), (5, 1, 4)])
+def test_sixteen_frame_passes_bit_identical(path, ty, kz):
+    """16-frame passes (stage 1 as two 8-frame halves, warp-row or one-pixel
+    loads; k_voxel16 with lane pairs) equal 8-frame passes bit for bit, for
+    several z-depths of the stage-2 tile."""
+    from paper_1311_6811_b200 import from_scene
+    s = make_scene("C2")
+    frames = np.stack([make_frames(s, f) for f in range(16)])
+    fr = torch.from_numpy(frames).cuda()
+    a = from_scene(s)
+    a.set_max_fuse(8)
+    b = from_scene(s)
+    b.set_max_fuse(16)
+    b.set_stage1_path(path)
+    b.set_voxel_tile(ty, kz)
+    La, Ba = a.alloc_outputs(16)
+    Lb, Bb = b.alloc_outputs(16)
+    a.reconstruct_batch(fr, 16, logodds=La, bits=Ba)
+    b.reconstruct_batch(fr, 16, logodds=Lb, bits=Bb)
+    torch.cuda.synchronize()
+    assert b.last_launch_count == 2  # one stage-1 and one stage-2 launch
+    assert torch.equal(Ba, Bb) and torch.equal(La, Lb)
+
+
 @pytest.mark.parametrize("ty,kz", [(1, 1), (4, 2), (1, 16)])
 def test_voxel_tile_shapes_bit_identical(ty, kz):
     from tests.helpers import gpu_run
@@ -101,18 +125,21 @@ def test_voxel_tile_shapes_bit_identical(ty, kz):
     assert torch.equal(Ba, Bb) and torch.equal(La, Lb)
 
 
-def test_overlapped_batches_bit_identical():
+@pytest.mark.parametrize("fuse", [8, 16])
+def test_overlapped_batches_bit_identical(fuse):
     """Stage 1 of group g+1 on the auxiliary stream beside stage 2 of group g
     (two term buffers) gives the same bits / log-odds as the serial schedule,
-    including mixed group sizes (21 = 8 + 8 + 4 + 1)."""
+    including mixed group sizes (21 = 8 + 8 + 4 + 1 or 16 + 4 + 1)."""
     from paper_1311_6811_b200 import from_scene
     s = make_scene("C2")
     frames = np.stack([make_frames(s, f % 16) for f in range(21)])
     fr = torch.from_numpy(frames).cuda()
     a = from_scene(s)
     a.set_overlap(False)
+    a.set_max_fuse(8)  # the serial reference always runs 8-frame passes
     b = from_scene(s)
     b.set_overlap(True, 2)
+    b.set_max_fuse(fuse)
     La, Ba = a.alloc_outputs(21)
     Lb, Bb = b.alloc_outputs(21)
     a.reconstruct_batch(fr, 21, logodds=La, bits=Ba)
@@ -122,27 +149,28 @@ def test_overlapped_batches_bit_identical():
     assert torch.equal(Ba, Bb) and torch.equal(La, Lb)
 
 
-@pytest.mark.parametrize("params", [dict(), dict(occlusion_prior=0.3, voxel_prior=0.2, threshold=0.7)])
-def test_carve_bits_identical(params):
+@pytest.mark.parametrize("params,nf", [(dict(), 8), (dict(), 16),
+                                       (dict(occlusion_prior=0.3, voxel_prior=0.2, threshold=0.7), 16)])
+def test_carve_bits_identical(params, nf):
     """psfs_set_carve: the bits-only early exit leaves the bitmask unchanged
-    (C2 skeleton frames and C1 with general priors), and is ignored when
-    log-odds are requested."""
+    (C2 skeleton frames and C1 with general priors; 8- and 16-frame passes),
+    and is ignored when log-odds are requested."""
     from paper_1311_6811_b200 import from_scene
     name = "C2" if not params else "C1"
     s = make_scene(name)
-    frames = np.stack([make_frames(s, f) for f in range(8)])
+    frames = np.stack([make_frames(s, f) for f in range(nf)])
     fr = torch.from_numpy(frames).cuda()
     a = from_scene(s, params)
     b = from_scene(s, params)
     b.set_carve(True)
-    _, Ba = a.alloc_outputs(8, logodds=False)
-    _, Bb = b.alloc_outputs(8, logodds=False)
-    a.reconstruct_batch(fr, 8, bits=Ba)
-    b.reconstruct_batch(fr, 8, bits=Bb)
-    Lc, Bc = b.alloc_outputs(8)
-    b.reconstruct_batch(fr, 8, logodds=Lc, bits=Bc)
-    La, Bd = a.alloc_outputs(8)
-    a.reconstruct_batch(fr, 8, logodds=La, bits=Bd)
+    _, Ba = a.alloc_outputs(nf, logodds=False)
+    _, Bb = b.alloc_outputs(nf, logodds=False)
+    a.reconstruct_batch(fr, nf, bits=Ba)
+    b.reconstruct_batch(fr, nf, bits=Bb)
+    Lc, Bc = b.alloc_outputs(nf)
+    b.reconstruct_batch(fr, nf, logodds=Lc, bits=Bc)
+    La, Bd = a.alloc_outputs(nf)
+    a.reconstruct_batch(fr, nf, logodds=La, bits=Bd)
     torch.cuda.synchronize()
     assert torch.equal(Ba, Bb)
     assert torch.equal(Bc, Bd) and torch.equal(Lc, La)

@@ -117,6 +117,24 @@ def test_c2_bench_configuration_batch_of_8():
     assert np.array_equal(g1["L"], g["L"][:3])
 
 
+def test_c2_batch_of_16_paired_kernel():
+    """16-frame passes (64-byte term records, lane pairs in k_voxel16): C2 with
+    16 distinct frames against the oracle, and bit-identical to 8-frame passes."""
+    s = make_scene("C2")
+    frames = [make_frames(s, f) for f in range(16)]
+    g, st = _parity(s, frames, fuse=16)
+    g8 = gpu_run(s, frames, fuse=8)
+    assert np.array_equal(g8["bits"], g["bits"])
+    assert np.array_equal(g8["L"], g["L"])
+
+
+def test_batch_grouping_29_frames():
+    """29 = 16 + 8 + 4 + 1 frames: every group size, against the oracle."""
+    s = make_scene("C1")
+    frames = [make_frames(s, f) for f in range(29)]
+    _parity(s, frames, fuse=16)
+
+
 def test_batch_grouping_13_frames():
     """13 = 8 + 4 + 1 frames: every group size path, against the oracle."""
     s = make_scene("C1")
@@ -138,17 +156,20 @@ def test_c3_sequence_frames():
     _parity(s, frames)
 
 
-def test_ragged_grid_and_images():
-    """xlen % 32 != 0 (atomic bit path), ylen % 8 != 0, zlen % KZ != 0, W % 4 != 0."""
+@pytest.mark.parametrize("nf,fuse", [(3, 8), (17, 16)])
+def test_ragged_grid_and_images(nf, fuse):
+    """xlen % 32 != 0 (atomic bit path), xlen odd (a lane pair with one voxel
+    outside the grid), ylen % 8 != 0, zlen % KZ != 0, W % 4 != 0."""
     g = Grid((-1000.0, -1000.0, 0.0), 2000.0 / 37, 37, 29, 23)
     s = make_scene("C1", grid=g, W=66, H=50)
-    _parity(s, [make_frames(s, f) for f in range(3)])
+    _parity(s, [make_frames(s, f) for f in range(nf)], fuse=fuse)
 
 
-def test_general_priors_and_threshold():
+@pytest.mark.parametrize("nf,fuse", [(2, 8), (16, 16)])
+def test_general_priors_and_threshold(nf, fuse):
     s = make_scene("C1")
     p = dict(occlusion_prior=0.3, voxel_prior=0.2, threshold=0.7, sigma_floor=1.5)
-    _parity(s, [make_frames(s, 0), make_frames(s, 1)], params=p)
+    _parity(s, [make_frames(s, f) for f in range(nf)], params=p, fuse=fuse)
 
 
 def test_all_background_gives_empty_hull():
