@@ -233,6 +233,41 @@ def run_reference(args):
 
 # ---------------------------------------------------------------- our arm
 
+def zslab_bench(args, scene, frames_dev, rank, world, local, dev, stream,
+                variants=(("fused_peer", True), ("nccl_allgather", False))):
+    """z-slab partition: every rank owns zlen/N slices of the
+    grid and the full bitmask reaches every rank.  Each rank uses its own 16
+    frames (timing only; tests/test_gpu_peer.py checks the exchanged bits)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1311_6811_b200.parallel import ZSlabReconstructor
+    nf = 16
+    fr = frames_dev[:nf].contiguous()
+    out = {"frames_per_call": nf, "slices_per_rank": scene.grid.zlen // world}
+    for name, peer in variants:
+        z = ZSlabReconstructor(scene, rank=rank, world=world, device=local, peer=peer,
+                               max_frames=nf)
+        bits = None if peer else torch.zeros((nf, scene.grid.nwords), dtype=torch.int32, device=dev)
+        for _ in range(args.warmup):
+            z.reconstruct_batch(fr, nf, bits=bits, stream=stream)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            z.reconstruct_batch(fr, nf, bits=bits, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if peer:
+            z.rec.peer_status(stream)
+        t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item()) / args.steps
+        out[name] = {"ms_per_call": ms, "frames_per_s": nf / (ms / 1e3)}
+        del z
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -466,6 +501,16 @@ def run_ours(args):
                  "note": "bits-only early exit (psfs_set_carve): a warp stops adding cameras once "
                          "its voxels are provably unoccupied; bitmask identical; not the headline"}
 
+    # ---- secondary (N > 1 only): z-slab partition of the same grid across the
+    # ranks, 16 frames per call, with the bitmask exchange fused into stage 2
+    # (peer stores + device barriers) and, for comparison, the NCCL all-gather
+    zslab = None
+    if world > 1 and not args.profile:
+        try:
+            zslab = zslab_bench(args, scene, frames_dev, rank, world, local, dev, stream)
+        except Exception as e:  # reported, never fatal for the headline
+            zslab = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+
     # ---- secondary: NEXT-2 surface extraction (psfs_surface) of one frame's bitmask
     surface = None
     if not args.profile:
@@ -532,7 +577,7 @@ def run_ours(args):
                                     if args.overlap >= 0 else "serial"),
                        "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the step events)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "carve": carve,
-            "surface": surface, "smooth": smooth,
+            "surface": surface, "smooth": smooth, "zslab": zslab,
             "gpu_launches": launches, "clocks": clocks,
             "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms),
                         "max": max(step_ms)},

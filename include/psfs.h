@@ -58,11 +58,14 @@ enum {
     PSFS_ESTATE = 5,      /* call order violated (cameras before backgrounds ...)  */
     PSFS_ECUDA = 6,       /* a CUDA runtime call or kernel launch failed           */
     PSFS_ENOMEM = 7,      /* device allocation failed                              */
-    PSFS_ELIMIT = 8       /* more cameras / frames than this build supports        */
+    PSFS_ELIMIT = 8,      /* more cameras / frames than this build supports        */
+    PSFS_ETIMEOUT = 9     /* a peer rank did not reach the exchange barrier        */
 };
 
 #define PSFS_MAX_CAMERAS 64 /* per handle                                  */
 #define PSFS_MAX_BATCH 16   /* frames fused into one stage-1/stage-2 pass  */
+#define PSFS_MAX_PEERS 8    /* ranks of one fused peer exchange (one node) */
+#define PSFS_IPC_HANDLE_BYTES 64 /* size of one exported peer buffer handle */
 
 typedef struct psfs_handle psfs_handle; /* opaque, library-owned */
 
@@ -87,7 +90,9 @@ typedef struct {
  * the handle computes slices [k0, k1) with k0 = rank*zlen/world; requires
  * zlen % world == 0 and xlen*ylen*(zlen/world) % 32 == 0 so every slab is a
  * whole number of bitmask words.  The bitmask exchange (all-gather) between
- * ranks is the caller's (NCCL through torch.distributed in the Python layer). */
+ * ranks is either the caller's (NCCL through torch.distributed in the Python
+ * layer) or fused into stage 2 (psfs_peer_alloc / psfs_peer_open /
+ * psfs_reconstruct_peer below). */
 typedef struct {
     int32_t device; /* CUDA device ordinal the handle allocates on            */
     int32_t rank;   /* 0 <= rank < world                                       */
@@ -235,6 +240,40 @@ int psfs_set_voxel_tile(psfs_handle *h, int32_t ty, int32_t kz);
  * A 16-frame pass stores 64-byte term records (two sectors of one 128-byte
  * line) that two lanes of k_voxel read together. */
 int psfs_set_max_fuse(psfs_handle *h, int32_t fmax);
+
+/* ---- Fused z-slab bitmask exchange over peer memory (DESIGN.md
+ * section 9).  Every rank of a z-slab partition (psfs_dist.world = N <= PSFS_MAX_PEERS,
+ * one process per GPU of one node, or several processes sharing one GPU) holds a
+ * library-owned buffer of nframes full-grid bitmasks; stage 2 stores each
+ * ballot byte of its slab into ALL N buffers (NVLink / NVSwitch peer stores
+ * through CUDA IPC mappings), so no separate all-gather runs, and a device-side
+ * barrier (release / acquire flags at system scope) orders the exchange on the
+ * caller's stream -- no host synchronisation.
+ *
+ * psfs_peer_alloc: allocate this rank's buffer for up to nframes frames;
+ *   *bits_out (HOST out) = its DEVICE address (nframes consecutive arrays of
+ *   ceil(nvox/32) words, valid after psfs_reconstruct_peer's barrier, owned by
+ *   the handle until psfs_destroy); ipc_handle_out (HOST, PSFS_IPC_HANDLE_BYTES)
+ *   = the handle to pass to every other rank (the caller moves it, e.g. with
+ *   torch.distributed.all_gather_object).  Errors: PSFS_EINVAL, PSFS_ELIMIT
+ *   (world > PSFS_MAX_PEERS), PSFS_ENOMEM, PSFS_ECUDA.
+ * psfs_peer_open: handles = HOST, world * PSFS_IPC_HANDLE_BYTES bytes in rank
+ *   order (this rank's own entry is ignored); maps every peer buffer.  Errors:
+ *   PSFS_ESTATE (no psfs_peer_alloc), PSFS_EINVAL, PSFS_ECUDA.
+ * psfs_reconstruct_peer: as psfs_reconstruct_batch (nframes <= the allocated
+ *   count) with bits going to every rank's buffer: entry barrier (every rank has
+ *   finished the work its stream ordered before this call, so no rank
+ *   overwrites a buffer still being read), both stages with peer stores, exit
+ *   barrier.  Every rank must make the same sequence of calls.  Asynchronous
+ *   on cuda_stream.  A barrier that waits more than ~10 s for a peer gives up
+ *   and records the failure, which psfs_peer_status reports.
+ * psfs_peer_status: synchronizes cuda_stream; PSFS_ETIMEOUT if a barrier timed
+ *   out since the last call, else PSFS_OK. */
+int psfs_peer_alloc(psfs_handle *h, int32_t nframes, uint32_t **bits_out, void *ipc_handle_out);
+int psfs_peer_open(psfs_handle *h, const void *handles);
+int psfs_reconstruct_peer(psfs_handle *h, int32_t nframes, const uint8_t *const *frames,
+                          float *logodds, void *cuda_stream);
+int psfs_peer_status(psfs_handle *h, void *cuda_stream);
 
 /* Per-kernel device timing (bench instrumentation): when enabled, every
  * stage-1 and stage-2 launch is bracketed by CUDA events on the launching

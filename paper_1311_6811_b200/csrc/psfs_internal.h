@@ -9,6 +9,7 @@ namespace psfs {
 constexpr int kMaxCam = 64;  // == PSFS_MAX_CAMERAS
 constexpr int kMaxF = 16;    // == PSFS_MAX_BATCH
 constexpr int kQBits = 20;   // Q11.20 fixed point for the per-view term t
+constexpr int kMaxPeers = 8; // == PSFS_MAX_PEERS
 
 // Background model of one pixel as stored on the device (set once by
 // psfs_set_background; K filled by k_prep_model): 32 bytes, so a row segment of
@@ -85,6 +86,22 @@ struct VParams {
     int32_t max_blocks_per_sm;         // 0: fill the SMs (occupancy); > 0: cap (overlap)
     int32_t carve;                     // bits-only early exit (no log-odds output)
     int32_t q_max;                     // largest possible term: rint(-ln p_O 2^20)
+    // fused z-slab exchange: npeer > 0 stores every bitmask byte into each rank's
+    // buffer, frame f of this group at peer[r] + f * peer_fstride (bits[] unused)
+    int32_t npeer;
+    uint32_t *peer[kMaxPeers];
+    int64_t peer_fstride;
+};
+
+// Device-side barrier of a fused exchange: flags[r] = rank r's flag array
+// (kMaxPeers uint64 slots, mapped in this process); this rank writes `epoch`
+// into slot `rank` of every rank's array, then waits for all `world` slots of
+// its own array to reach `epoch` (err = 1 after a ~10 s timeout).
+struct PeerBarrier {
+    unsigned long long *flags[kMaxPeers];
+    int32_t rank, world;
+    unsigned long long epoch;
+    int *err;
 };
 
 // Launchers (psfs_kernels.cu).  Return the cudaError_t of the launch.
@@ -98,6 +115,7 @@ cudaError_t launch_surface(const uint32_t *bits, uint32_t *surf, int64_t *idx, i
 int surface_blocks(int xlen, int ylen, int k0, int k1);
 cudaError_t launch_smooth(const float *logodds, float *P, float *smoothed, uint32_t *bits, int xlen,
                           int ylen, int zlen, float tau, cudaStream_t s);
+cudaError_t launch_peer_barrier(const PeerBarrier &b, cudaStream_t s);
 cudaError_t launch_l1_probe(const void *buf, int blocks, int iters, int *out, cudaStream_t s);
 cudaError_t launch_rcp_check(uint32_t lo_bits, uint32_t hi_bits, unsigned long long *bad,
                              cudaStream_t s);

@@ -10,8 +10,14 @@ One process per GPU (torchrun), torch.distributed for the plumbing:
 * z-slab (config C4): rank r owns slices [r*zlen/N, (r+1)*zlen/N) of the grid
   (the library's psfs_dist), runs stage 1 only on the pixel rectangle its slab
   projects into, stage 2 on its slab, and the full occupancy bitmask is
-  assembled on every rank by one in-place all-gather of the per-slab words
-  (NCCL over NVLink on GPUs; gloo in the CPU tests).  Log-odds stay sharded.
+  assembled on every rank either
+  - fused (peer=True, the default on GPUs of one node): stage 2 stores each
+    ballot byte of the slab into every rank's exchange buffer through CUDA IPC
+    peer mappings (NVLink / NVSwitch), ordered by device-side barriers --
+    no separate collective; torch.distributed only moves the IPC handles once;
+  - or by one in-place all-gather of the per-slab words (NCCL over NVLink on
+    GPUs; gloo in the CPU tests).
+  Log-odds stay sharded.
 
 The slab rule here is the same pure function the library applies
 (k0 = zlen*rank//world); tests check both agree.
@@ -75,10 +81,22 @@ def env_rank_world():
     return rank, world, local
 
 
-class ZSlabReconstructor:
-    """A z-slab handle plus the bitmask all-gather (NCCL process group)."""
+def exchange_handles(handle: bytes, world: int, group=None):
+    """All-gather one IPC handle per rank (host objects; any backend)."""
+    import torch.distributed as dist
+    if world == 1:
+        return [handle]
+    out = [None] * world
+    dist.all_gather_object(out, handle, group=group)
+    return out
 
-    def __init__(self, scene, params=None, rank=None, world=None, device=None, group=None):
+
+class ZSlabReconstructor:
+    """A z-slab handle plus the bitmask exchange: fused peer stores (peer=True)
+    or an NCCL all-gather of the slab words (peer=False)."""
+
+    def __init__(self, scene, params=None, rank=None, world=None, device=None, group=None,
+                 peer=False, max_frames=16):
         from .psfs import from_scene
         r, w, local = env_rank_world()
         self.rank = r if rank is None else rank
@@ -89,10 +107,39 @@ class ZSlabReconstructor:
         self.group = group
         self.rec = from_scene(scene, params, device=local if device is None else device,
                               rank=self.rank, world=self.world)
+        self.peer = peer
+        self.bits = None
+        if peer:
+            # host collectives at setup only: every rank maps every other rank's
+            # buffer; a failure on any rank makes every rank raise (no rank is
+            # left waiting in a collective or a device barrier)
+            try:
+                self.bits, h = self.rec.peer_alloc(max_frames)
+            except Exception:
+                h = b""
+            handles = exchange_handles(h, self.world, group)
+            if any(not x for x in handles):
+                raise RuntimeError("psfs_peer_alloc failed on rank(s) "
+                                   f"{[r for r, x in enumerate(handles) if not x]}")
+            try:
+                self.rec.peer_open(handles)
+                ok = b"1"
+            except Exception:
+                ok = b""
+            oks = exchange_handles(ok, self.world, group)
+            if not all(oks):
+                raise RuntimeError("psfs_peer_open failed on rank(s) "
+                                   f"{[r for r, x in enumerate(oks) if not x]}")
 
     def reconstruct_batch(self, frames, nframes, logodds=None, bits=None, stream=None,
                           gather=True):
+        """peer mode: the full-grid bitmasks land in self.bits[:nframes] on every
+        rank (stream-ordered, no host synchronisation); `bits` is ignored."""
+        if self.peer:
+            self.rec.reconstruct_peer(frames, nframes, logodds=logodds, stream=stream)
+            return self.bits[:nframes]
         self.rec.reconstruct_batch(frames, nframes, logodds=logodds, bits=bits, stream=stream)
         if gather and bits is not None:
             g = self.grid
             allgather_bits(bits, g.xlen, g.ylen, g.zlen, self.world, self.rank, self.group)
+        return bits

@@ -22,9 +22,12 @@ LIB_PATH = os.environ.get("PSFS_LIB", os.path.join(_HERE, "libpsfs.so"))
 
 PSFS_OK = 0
 STATUS = {0: "PSFS_OK", 1: "PSFS_EINVAL", 2: "PSFS_EDEGENERATE", 3: "PSFS_EDIM", 4: "PSFS_ECOUNT",
-          5: "PSFS_ESTATE", 6: "PSFS_ECUDA", 7: "PSFS_ENOMEM", 8: "PSFS_ELIMIT"}
+          5: "PSFS_ESTATE", 6: "PSFS_ECUDA", 7: "PSFS_ENOMEM", 8: "PSFS_ELIMIT",
+          9: "PSFS_ETIMEOUT"}
 MAX_CAMERAS = 64
 MAX_BATCH = 16
+MAX_PEERS = 8
+IPC_HANDLE_BYTES = 64
 
 # Every symbol include/psfs.h declares (checked by tests/test_abi.py).
 EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_background",
@@ -34,7 +37,8 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_last_launch_count", "psfs_set_profiling", "psfs_kernel_times",
            "psfs_fast_rcp_enabled", "psfs_debug_rcp_check", "psfs_probe_l1_bandwidth",
            "psfs_set_stage1_path", "psfs_set_voxel_tile", "psfs_set_overlap",
-           "psfs_set_carve", "psfs_surface", "psfs_smooth_threshold"]
+           "psfs_set_carve", "psfs_surface", "psfs_smooth_threshold", "psfs_peer_alloc",
+           "psfs_peer_open", "psfs_reconstruct_peer", "psfs_peer_status"]
 
 
 class PsfsError(RuntimeError):
@@ -101,6 +105,10 @@ def lib():
         L.psfs_fast_rcp_enabled.argtypes = [vp]
         L.psfs_debug_rcp_check.argtypes = [C.c_float, C.c_float, C.POINTER(C.c_int64)]
         L.psfs_probe_l1_bandwidth.argtypes = [C.POINTER(C.c_double)]
+        L.psfs_peer_alloc.argtypes = [vp, i32, C.POINTER(vp), vp]
+        L.psfs_peer_open.argtypes = [vp, vp]
+        L.psfs_reconstruct_peer.argtypes = [vp, i32, vp, vp, vp]
+        L.psfs_peer_status.argtypes = [vp, vp]
         _lib = L
     return _lib
 
@@ -290,6 +298,52 @@ class Reconstructor:
             raise ValueError("bits too small")
         self._check(lib().psfs_reconstruct_batch(self._h, int(nframes), fp, Lp, Bp, s),
                     "psfs_reconstruct_batch")
+
+    # -- fused z-slab exchange (include/psfs.h psfs_peer_*) --------------------
+    def peer_alloc(self, nframes: int):
+        """Allocate this rank's exchange buffer (nframes full-grid bitmasks);
+        returns (bits int32 CUDA tensor [nframes, nwords] viewing it, the
+        IPC handle bytes to hand to every other rank)."""
+        import torch
+        ptr = C.c_void_p()
+        hbuf = C.create_string_buffer(IPC_HANDLE_BYTES)
+        self._check(lib().psfs_peer_alloc(self._h, int(nframes), C.byref(ptr), hbuf),
+                    "psfs_peer_alloc")
+        nwords = self.grid.nwords
+
+        class _View:  # __cuda_array_interface__ over the library-owned buffer
+            __cuda_array_interface__ = {"shape": (int(nframes), nwords), "typestr": "<i4",
+                                        "data": (int(ptr.value), False), "version": 2,
+                                        "strides": None}
+        with torch.cuda.device(self.device):
+            bits = torch.as_tensor(_View(), device=torch.device("cuda", self.device))
+        self._peer_bits = bits
+        return bits, hbuf.raw
+
+    def peer_open(self, handles):
+        """handles: list of world IPC handle byte strings in rank order."""
+        if len(handles) != self.world or any(len(x) != IPC_HANDLE_BYTES for x in handles):
+            raise ValueError("need world handles of IPC_HANDLE_BYTES each")
+        buf = C.create_string_buffer(b"".join(handles), IPC_HANDLE_BYTES * self.world)
+        self._check(lib().psfs_peer_open(self._h, buf), "psfs_peer_open")
+
+    def reconstruct_peer(self, frames, nframes: int, logodds=None, stream=None):
+        """Both stages with the bitmask bytes stored into every rank's exchange
+        buffer, between device-side entry and exit barriers (all ranks call it)."""
+        import torch
+        fp = self._frame_ptrs(frames, nframes)
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        if logodds is not None and logodds.numel() < nframes * self.nslab:
+            raise ValueError("logodds too small")
+        self._check(lib().psfs_reconstruct_peer(self._h, int(nframes), fp,
+                                                _dev_ptr(logodds, torch.float32), s),
+                    "psfs_reconstruct_peer")
+
+    def peer_status(self, stream=None):
+        """Synchronize and raise PsfsError(PSFS_ETIMEOUT) if a barrier timed out."""
+        import torch
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._check(lib().psfs_peer_status(self._h, s), "psfs_peer_status")
 
     def reconstruct(self, frames, logodds=None, bits=None, stream=None):
         import torch

@@ -96,3 +96,33 @@ def test_zslab_allgather_assembles_full_grid(world):
         full = oracle.scene_reconstruct(s, make_frames(s, f))["bits"].view(np.int32)
         for r in range(world):
             assert np.array_equal(results[r][f], full), (r, f)
+
+
+def _handles_worker(rank, world, port, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        h = bytes([rank]) * 64  # stands in for this rank's cudaIpcMemHandle_t
+        result_q.put((rank, parallel.exchange_handles(h, world)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_exchange_handles_rank_order(world):
+    """The fused exchange's one host collective: every rank receives every
+    rank's IPC handle, in rank order (what psfs_peer_open expects)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_handles_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [bytes([r]) * 64 for r in range(world)]
+    for r in range(world):
+        assert results[r] == want
