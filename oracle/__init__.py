@@ -69,6 +69,8 @@ def lib():
         _lib.oracle_surface.argtypes = [vp, C.POINTER(_Grid), i, i, vp, i64]
         _lib.oracle_surface.restype = i64
         _lib.oracle_smooth_threshold.argtypes = [vp, C.POINTER(_Grid), d, vp, vp]
+        _lib.oracle_color.argtypes = [C.POINTER(_Rig), C.POINTER(_Grid), vp, vp, vp, d, d, i64,
+                                      vp, vp, vp, vp]
     return _lib
 
 
@@ -224,6 +226,28 @@ def fuse_sample(P, W, H, grid, frames, mu, sigma, vox, sigma_floor=1.0, p_occ=0.
                              _p(_ptrs(sg)), float(sigma_floor), float(p_vox), vox.shape[0],
                              _p(vox), _p(L), _p(post), int(nthreads))
     return L, post
+
+
+def color(P, W, H, grid, frames, mu, sigma, vox, slm_gate=0.5, sigma_floor=1.0, p_occ=0.5):
+    """NEXT-4: per listed voxel, the mean
+    8-bit RGB over the cameras whose pinned nearest pixel is in view and has
+    SLM > slm_gate.  Returns (rgb float64 [n, 3] (0 where unset), count int32
+    [n], margin float64 [n] = min |SLM - slm_gate| over the in-view cameras)."""
+    A = precompose(P, grid.origin, grid.spacing)
+    rh = _RigHolder(A, W, H, p_occ)
+    g = _grid(grid)
+    fr = [np.ascontiguousarray(f, np.uint8) for f in frames]
+    mu = [np.ascontiguousarray(m, np.float32) for m in mu]
+    sg = [np.ascontiguousarray(s, np.float32) for s in sigma]
+    vox = np.ascontiguousarray(np.asarray(vox, np.int64))
+    n = vox.shape[0]
+    rgb = np.empty((n, 3), np.float64)
+    cnt = np.empty(n, np.int32)
+    margin = np.empty(n, np.float64)
+    lib().oracle_color(C.byref(rh.rig), C.byref(g), _p(_ptrs(fr)), _p(_ptrs(mu)), _p(_ptrs(sg)),
+                       float(sigma_floor), float(slm_gate), n, _p(vox), _p(rgb), _p(cnt),
+                       _p(margin))
+    return rgb, cnt, margin
 
 
 def projection_flips(P, W, H, grid, k0=0, k1=None, p_occ=0.5, nthreads=1) -> int:

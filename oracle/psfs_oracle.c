@@ -388,6 +388,49 @@ void oracle_smooth_threshold(const double *post, const oracle_grid *g, double ta
             }
 }
 
+/* ------------------------------------------------------------------------ */
+/* NEXT-4: voxel colour ("the color rendering is also an iterative      */
+/* process of all voxels", "Voxel color calculation",        */
+/* P:303-307).  For each listed voxel: over the cameras whose      */
+/* pinned nearest pixel is in view (R#10-R#12) and whose SLM there (Eq 1-2)    */
+/* exceeds slm_gate (default 1/2; R#24), the arithmetic mean of the     */
+/* 8-bit RGB at that pixel (R#23); no occlusion test.  count = number */
+/* of qualifying views (0: colour unset, rgb = 0).  margin = the smallest      */
+/* |SLM - slm_gate| over the in-view cameras (the parity band).               */
+/* ------------------------------------------------------------------------ */
+void oracle_color(const oracle_rig *rig, const oracle_grid *g, const uint8_t *const *frames,
+                  const float *const *mu, const float *const *sigma, double sigma_floor,
+                  double slm_gate, int64_t n, const int64_t *vox, double *rgb_out,
+                  int32_t *count_out, double *margin_out)
+{
+    for (int64_t s = 0; s < n; ++s) {
+        const int64_t v = vox[s];
+        const int i = (int)(v % g->xlen);
+        const int j = (int)((v / g->xlen) % g->ylen);
+        const int k = (int)(v / ((int64_t)g->xlen * g->ylen));
+        double sum[3] = {0.0, 0.0, 0.0}, margin = INFINITY;
+        int32_t cnt = 0;
+        for (int c = 0; c < rig->ncam; ++c) {
+            int px, py;
+            if (!oracle_project_pinned(rig->A + 12 * c, rig->W[c], rig->H[c], i, j, k, &px, &py))
+                continue;
+            const int64_t p = (int64_t)py * rig->W[c] + px;
+            const uint8_t *I = frames[c] + 3 * p;
+            double slm;
+            oracle_pixel(I, mu[c] + 3 * p, sigma[c] + 3 * p, sigma_floor, rig->p_occ, &slm, NULL,
+                         NULL);
+            if (fabs(slm - slm_gate) < margin) margin = fabs(slm - slm_gate);
+            if (slm > slm_gate) {
+                for (int ch = 0; ch < 3; ++ch) sum[ch] += (double)I[ch];
+                ++cnt;
+            }
+        }
+        for (int ch = 0; ch < 3; ++ch) rgb_out[3 * s + ch] = cnt ? sum[ch] / cnt : 0.0;
+        count_out[s] = cnt;
+        if (margin_out) margin_out[s] = margin;
+    }
+}
+
 int oracle_max_threads(void)
 {
 #ifdef _OPENMP

@@ -43,6 +43,10 @@ int64_t oracle_surface(const uint32_t *bits, const oracle_grid *g, int k0, int k
                        int64_t capacity);
 void oracle_smooth_threshold(const double *post, const oracle_grid *g, double tau, double *smoothed,
                              uint32_t *bits_out);
+void oracle_color(const oracle_rig *rig, const oracle_grid *g, const uint8_t *const *frames,
+                  const float *const *mu, const float *const *sigma, double sigma_floor,
+                  double slm_gate, int64_t n, const int64_t *vox, double *rgb_out,
+                  int32_t *count_out, double *margin_out);
 int oracle_max_threads(void);
 
 #endif
