@@ -233,6 +233,31 @@ def run_reference(args):
 
 # ---------------------------------------------------------------- our arm
 
+def device_us(fn, dev, reps=20):
+    """Device time of one fn() call (µs): fn's launches captured once in a CUDA
+    graph and replayed `reps` times between CUDA events, so Python / ctypes
+    launch overhead (tens of µs per call) is not what is measured."""
+    import torch
+    s = torch.cuda.Stream(dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(s):
+        fn(s)  # warm-up outside the capture (lazy scratch allocations)
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        fn(s)
+    g.replay()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        e0.record(s)
+        for _ in range(reps):
+            g.replay()
+        e1.record(s)
+    torch.cuda.synchronize(dev)
+    return e0.elapsed_time(e1) / reps * 1e3
+
+
 def zslab_bench(args, scene, frames_dev, rank, world, local, dev, stream,
                 variants=(("fused_peer", True), ("nccl_allgather", False))):
     """z-slab partition: every rank owns zlen/N slices of the
@@ -517,20 +542,35 @@ def run_ours(args):
         cnt = torch.zeros(1, dtype=torch.int64, device=dev)
         idx = torch.empty(nvox, dtype=torch.int64, device=dev)
         sbits = torch.empty_like(Bits[0])
-        for _ in range(3):
-            rec.surface(Bits[0], surface_bits=sbits, indices=idx, count=cnt, stream=stream)
-        torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(20):
-            rec.surface(Bits[0], surface_bits=sbits, indices=idx, count=cnt, stream=stream)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        surface = {"us_per_frame": e0.elapsed_time(e1) / 20 * 1e3, "surface_voxels": int(cnt.item()),
+        us = device_us(lambda st: rec.surface(Bits[0], surface_bits=sbits, indices=idx, count=cnt,
+                                              stream=st), dev)
+        surface = {"us_per_frame": us, "surface_voxels": int(cnt.item()),
                    "occupied_voxels": int(torch.bitwise_and(
                        Bits[0].view(-1, 1) >> torch.arange(32, device=dev, dtype=torch.int32), 1).sum().item()),
                    "note": "NEXT-2 inner-voxel removal (P:301): bit-parallel 6-neighbour test + ordered "
-                           "compaction, 3 launches, not part of the headline step"}
+                           "compaction, 3 launches (device time, CUDA-graph replay), not part of the "
+                           "headline step"}
+
+    # ---- secondary: NEXT-4 voxel colour (psfs_color) of one frame's surface voxels,
+    # chained on the device after psfs_surface (count never read on the host)
+    color = None
+    if not args.profile:
+        _, Bc = rec.alloc_outputs(1, logodds=False)
+        rec.reconstruct(frames_dev[0], bits=Bc, stream=stream)
+        ccnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        cidx = torch.empty(nvox, dtype=torch.int64, device=dev)
+        rec.surface(Bc[0], indices=cidx, count=ccnt, stream=stream)
+        crgb = torch.empty((nvox, 3), dtype=torch.float32, device=dev)
+        cnv = torch.empty(nvox, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize(dev)
+        us = device_us(lambda st: rec.color(frames_dev[0], cidx, count=ccnt, rgb=crgb, nviews=cnv,
+                                            stream=st), dev)
+        nsurf = int(ccnt.item())
+        color = {"us_per_frame": us, "surface_voxels": nsurf,
+                 "coloured_voxels": int((cnv[:nsurf] > 0).sum().item()),
+                 "note": "NEXT-4 voxel colour (P:222, P:273-275): mean RGB over in-view cameras "
+                         "with SLM > 1/2 at each surface voxel, 1 launch (device time, CUDA-graph "
+                         "replay), not part of the headline step"}
 
     # ---- secondary: NEXT-1 merged filtering + thresholding (psfs_smooth_threshold)
     smooth = None
@@ -539,16 +579,9 @@ def run_ours(args):
         rec.reconstruct(frames_dev[0], logodds=Lf, bits=Bf, stream=stream)
         smv = torch.empty_like(Lf[0])
         smb = torch.empty_like(Bf[0])
-        for _ in range(3):
-            rec.smooth_threshold(Lf[0], smoothed=smv, bits=smb, stream=stream)
         torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(20):
-            rec.smooth_threshold(Lf[0], smoothed=smv, bits=smb, stream=stream)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        smooth = {"us_per_frame": e0.elapsed_time(e1) / 20 * 1e3,
+        us = device_us(lambda st: rec.smooth_threshold(Lf[0], smoothed=smv, bits=smb, stream=st), dev)
+        smooth = {"us_per_frame": us,
                   "note": "NEXT-1 posterior 3x3x3 box filter + threshold (P:111, P:300), "
                           "2 launches, not part of the headline step"}
 
@@ -577,7 +610,7 @@ def run_ours(args):
                                     if args.overlap >= 0 else "serial"),
                        "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the step events)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "carve": carve,
-            "surface": surface, "smooth": smooth, "zslab": zslab,
+            "surface": surface, "color": color, "smooth": smooth, "zslab": zslab,
             "gpu_launches": launches, "clocks": clocks,
             "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms),
                         "max": max(step_ms)},

@@ -241,6 +241,23 @@ int psfs_set_voxel_tile(psfs_handle *h, int32_t ty, int32_t kz);
  * line) that two lanes of k_voxel read together. */
 int psfs_set_max_fuse(psfs_handle *h, int32_t fmax);
 
+/* NEXT-4, voxel colour ("the color rendering is also an iterative
+ * process of all voxels", "Voxel color calculation"):
+ * for each listed voxel, the mean 8-bit RGB of one frame set over the cameras
+ * whose pinned nearest pixel (R#10-R#13, as the occupancy path) is in view and
+ * whose SLM there (Eq 1-2) exceeds slm_gate (0.5 by default, in (0,1);
+ * DESIGN.md R#23-R#24); no occlusion test.  frames: HOST array of ncam
+ * DEVICE pointers (one frame set).  indices: DEVICE int64 linear voxel indices
+ * (e.g. psfs_surface's list); count: DEVICE, one int64 -- min(*count, capacity)
+ * entries are coloured, so psfs_surface's outputs chain without a host sync.
+ * rgb: DEVICE, capacity x 3 float (0 when unset); nviews: DEVICE, nullable,
+ * capacity int32 qualifying views (0: colour unset, -1: index outside the grid).
+ * Asynchronous on cuda_stream.  Errors: PSFS_EINVAL, PSFS_ESTATE, PSFS_ECOUNT,
+ * PSFS_ECUDA. */
+int psfs_color(psfs_handle *h, const uint8_t *const *frames, const int64_t *indices,
+               const int64_t *count, int64_t capacity, double slm_gate, float *rgb,
+               int32_t *nviews, void *cuda_stream);
+
 /* ---- Fused z-slab bitmask exchange over peer memory (DESIGN.md
  * section 9).  Every rank of a z-slab partition (psfs_dist.world = N <= PSFS_MAX_PEERS,
  * one process per GPU of one node, or several processes sharing one GPU) holds a

@@ -93,6 +93,27 @@ struct VParams {
     int64_t peer_fstride;
 };
 
+// NEXT-4 voxel colour (psfs_color): per camera the pinned matrix, the image and
+// the model records of its pixels.
+struct ColorCam {
+    float A[12];
+    int32_t W, H;
+    int64_t off;              // first model record of this camera
+    const uint8_t *frame;     // H*W*3 RGB (device)
+};
+
+struct ColorParams {
+    ColorCam cam[kMaxCam];
+    const struct ModelPx *model;
+    const int64_t *indices;   // linear voxel indices (device)
+    const int64_t *count;     // device: number of valid indices (min with capacity)
+    int64_t capacity;
+    float *rgb;               // n x 3 (device)
+    int32_t *nviews;          // n (device, nullable)
+    double d_gate;            // a view qualifies iff d < d_gate (SLM > gate)
+    int32_t ncam, xlen, ylen, zlen;
+};
+
 // Device-side barrier of a fused exchange: flags[r] = rank r's flag array
 // (kMaxPeers uint64 slots, mapped in this process); this rank writes `epoch`
 // into slot `rank` of every rank's array, then waits for all `world` slots of
@@ -116,6 +137,7 @@ int surface_blocks(int xlen, int ylen, int k0, int k1);
 cudaError_t launch_smooth(const float *logodds, float *P, float *smoothed, uint32_t *bits, int xlen,
                           int ylen, int zlen, float tau, cudaStream_t s);
 cudaError_t launch_peer_barrier(const PeerBarrier &b, cudaStream_t s);
+cudaError_t launch_color(const ColorParams &p, cudaStream_t s);
 cudaError_t launch_l1_probe(const void *buf, int blocks, int iters, int *out, cudaStream_t s);
 cudaError_t launch_rcp_check(uint32_t lo_bits, uint32_t hi_bits, unsigned long long *bad,
                              cudaStream_t s);

@@ -38,7 +38,7 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_fast_rcp_enabled", "psfs_debug_rcp_check", "psfs_probe_l1_bandwidth",
            "psfs_set_stage1_path", "psfs_set_voxel_tile", "psfs_set_overlap",
            "psfs_set_carve", "psfs_surface", "psfs_smooth_threshold", "psfs_peer_alloc",
-           "psfs_peer_open", "psfs_reconstruct_peer", "psfs_peer_status"]
+           "psfs_peer_open", "psfs_reconstruct_peer", "psfs_peer_status", "psfs_color"]
 
 
 class PsfsError(RuntimeError):
@@ -109,6 +109,7 @@ def lib():
         L.psfs_peer_open.argtypes = [vp, vp]
         L.psfs_reconstruct_peer.argtypes = [vp, i32, vp, vp, vp]
         L.psfs_peer_status.argtypes = [vp, vp]
+        L.psfs_color.argtypes = [vp, vp, vp, vp, C.c_int64, d, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -422,6 +423,28 @@ class Reconstructor:
         out = np.empty((self.ncam, 4), np.int32)
         self._check(lib().psfs_debug_roi(self._h, out.ctypes.data), "psfs_debug_roi")
         return out
+
+    def color(self, frames, indices, count=None, rgb=None, nviews=None, slm_gate=0.5, stream=None):
+        """NEXT-4 voxel colour of one frame set ([ncam, H, W, 3] uint8 CUDA
+        tensor) at int64 CUDA `indices`; count: optional int64 CUDA tensor [1]
+        (e.g. from surface()), else all of `indices`.  Returns (rgb float32
+        [capacity, 3], nviews int32 [capacity]) CUDA tensors."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        cap = int(indices.numel())
+        if count is None:
+            count = torch.tensor([cap], dtype=torch.int64, device=dev)
+        if rgb is None:
+            rgb = torch.empty((cap, 3), dtype=torch.float32, device=dev)
+        if nviews is None:
+            nviews = torch.empty(cap, dtype=torch.int32, device=dev)
+        fp = self._frame_ptrs(frames, 1)
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._check(lib().psfs_color(self._h, fp, _dev_ptr(indices, torch.int64),
+                                     _dev_ptr(count, torch.int64), cap, float(slm_gate),
+                                     _dev_ptr(rgb, torch.float32), _dev_ptr(nviews, torch.int32),
+                                     s), "psfs_color")
+        return rgb, nviews
 
     def set_profiling(self, on: bool):
         self._check(lib().psfs_set_profiling(self._h, int(bool(on))), "psfs_set_profiling")
