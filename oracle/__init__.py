@@ -71,6 +71,7 @@ def lib():
         _lib.oracle_smooth_threshold.argtypes = [vp, C.POINTER(_Grid), d, vp, vp]
         _lib.oracle_color.argtypes = [C.POINTER(_Rig), C.POINTER(_Grid), vp, vp, vp, d, d, i64,
                                       vp, vp, vp, vp]
+        _lib.oracle_train_background.argtypes = [i, i64, vp, d, vp, vp]
     return _lib
 
 
@@ -248,6 +249,22 @@ def color(P, W, H, grid, frames, mu, sigma, vox, slm_gate=0.5, sigma_floor=1.0, 
                        float(sigma_floor), float(slm_gate), n, _p(vox), _p(rgb), _p(cnt),
                        _p(margin))
     return rgb, cnt, margin
+
+
+def train_background(frames, sigma_floor=1.0):
+    """NEXT-3: per-pixel, per-channel mean and population standard
+    deviation of a list of [H, W, 3] uint8 frames, sigma clamped to the floor.
+    Returns (mean, sigma) float64 [H, W, 3]."""
+    fr = [np.ascontiguousarray(f, np.uint8) for f in frames]
+    if not fr:
+        raise ValueError("EmptyInput")
+    if any(f.shape != fr[0].shape for f in fr):
+        raise ValueError("DimensionMismatch")
+    npx = fr[0].size // 3
+    mean = np.empty(fr[0].shape, np.float64)
+    sd = np.empty(fr[0].shape, np.float64)
+    lib().oracle_train_background(len(fr), npx, _p(_ptrs(fr)), float(sigma_floor), _p(mean), _p(sd))
+    return mean, sd
 
 
 def projection_flips(P, W, H, grid, k0=0, k1=None, p_occ=0.5, nthreads=1) -> int:

@@ -431,6 +431,31 @@ void oracle_color(const oracle_rig *rig, const oracle_grid *g, const uint8_t *co
     }
 }
 
+/* ------------------------------------------------------------------------ */
+/* NEXT-3: background-model training (the paper assumes mu, sigma   */
+/* exist).  Per pixel and channel over n frames: the sample mean and    */
+/* the population standard deviation, sigma clamped up to the floor   */
+/* (R#6).  Two passes in double.                                       */
+/* ------------------------------------------------------------------------ */
+void oracle_train_background(int n, int64_t npx, const uint8_t *const *frames, double sigma_floor,
+                             double *mean_out, double *sigma_out)
+{
+    for (int64_t e = 0; e < 3 * npx; ++e) {
+        double sum = 0.0;
+        for (int f = 0; f < n; ++f) sum += (double)frames[f][e];
+        const double mean = sum / n;
+        double ss = 0.0;
+        for (int f = 0; f < n; ++f) {
+            const double dv = (double)frames[f][e] - mean;
+            ss += dv * dv;
+        }
+        double sd = sqrt(ss / n);
+        if (sd < sigma_floor) sd = sigma_floor;
+        mean_out[e] = mean;
+        sigma_out[e] = sd;
+    }
+}
+
 int oracle_max_threads(void)
 {
 #ifdef _OPENMP

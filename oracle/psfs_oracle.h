@@ -47,6 +47,8 @@ void oracle_color(const oracle_rig *rig, const oracle_grid *g, const uint8_t *co
                   const float *const *mu, const float *const *sigma, double sigma_floor,
                   double slm_gate, int64_t n, const int64_t *vox, double *rgb_out,
                   int32_t *count_out, double *margin_out);
+void oracle_train_background(int n, int64_t npx, const uint8_t *const *frames, double sigma_floor,
+                             double *mean_out, double *sigma_out);
 int oracle_max_threads(void);
 
 #endif
