@@ -572,6 +572,19 @@ def run_ours(args):
                          "with SLM > 1/2 at each surface voxel, 1 launch (device time, CUDA-graph "
                          "replay), not part of the headline step"}
 
+    # ---- secondary: NEXT-3 background training (psfs_train_background) of one
+    # camera from 32 frames, outputs only (the bench's model stays installed)
+    train = None
+    if not args.profile:
+        tf = frames_dev[:32, 0].contiguous()
+        us = device_us(lambda st: rec.train_background(0, tf, install=False, stream=st), dev)
+        tbytes = tf.numel() + 2 * 4 * tf[0].numel()
+        train = {"us_per_camera": us, "frames": int(tf.shape[0]),
+                 "achieved_gbs": tbytes / (us * 1e-6) / 1e9,
+                 "note": "NEXT-3 background training (S:99-107): per-pixel mean and population "
+                         "std over 32 frames of one 640x480 camera, 1 launch (device time, "
+                         "CUDA-graph replay); bytes = frames read + mean/sigma written"}
+
     # ---- secondary: NEXT-1 merged filtering + thresholding (psfs_smooth_threshold)
     smooth = None
     if not args.profile:
@@ -610,7 +623,7 @@ def run_ours(args):
                                     if args.overlap >= 0 else "serial"),
                        "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the step events)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "carve": carve,
-            "surface": surface, "color": color, "smooth": smooth, "zslab": zslab,
+            "surface": surface, "color": color, "smooth": smooth, "train": train, "zslab": zslab,
             "gpu_launches": launches, "clocks": clocks,
             "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms),
                         "max": max(step_ms)},

@@ -65,6 +65,7 @@ enum {
 #define PSFS_MAX_CAMERAS 64 /* per handle                                  */
 #define PSFS_MAX_BATCH 16   /* frames fused into one stage-1/stage-2 pass  */
 #define PSFS_MAX_PEERS 8    /* ranks of one fused peer exchange (one node) */
+#define PSFS_MAX_TRAIN_FRAMES 512 /* frames of one psfs_train_background call */
 #define PSFS_IPC_HANDLE_BYTES 64 /* size of one exported peer buffer handle */
 
 typedef struct psfs_handle psfs_handle; /* opaque, library-owned */
@@ -125,6 +126,21 @@ int psfs_set_cameras(psfs_handle *h, int32_t ncam, const double *P, const int32_
  * camera's), PSFS_ECUDA. */
 int psfs_set_background(psfs_handle *h, int32_t cam, int32_t width, int32_t height,
                         const float *mean, const float *sigma);
+
+/* NEXT-3, background-model training (the paper assumes the single
+ * Gaussian of P:77 exists): camera `cam`'s per-pixel, per-channel sample mean
+ * and population standard deviation over nframes background frames, sigma
+ * clamped up to sigma_floor (R#6).  frames: HOST array of nframes
+ * DEVICE pointers, each an H_c*W_c*3 uint8 image.  mean / sigma: DEVICE,
+ * nullable, H_c*W_c*3 float (sigma after the clamp).  install != 0 makes the
+ * result camera cam's background model, exactly as psfs_set_background with
+ * these float values would, without a host round trip.  Asynchronous on
+ * cuda_stream.  Errors: PSFS_ESTATE (no cameras), PSFS_EINVAL (cam out of
+ * range, nframes <= 0 = EmptyInput of S:104, NULL frame, no output),
+ * PSFS_ELIMIT (nframes > PSFS_MAX_TRAIN_FRAMES), PSFS_ECUDA. */
+int psfs_train_background(psfs_handle *h, int32_t cam, int32_t nframes,
+                          const uint8_t *const *frames, float *mean, float *sigma, int32_t install,
+                          void *cuda_stream);
 
 /* Reconstruct one frame set.  frames: HOST array of ncam DEVICE pointers, each
  * an H_c*W_c*3 uint8 RGB image (row-major, channel-interleaved).

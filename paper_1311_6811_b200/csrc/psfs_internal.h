@@ -128,6 +128,18 @@ struct PeerBarrier {
 // Launchers (psfs_kernels.cu).  Return the cudaError_t of the launch.
 cudaError_t launch_likelihood(const S1Params &p, int F, int max_roi_px, int path, cudaStream_t s);
 cudaError_t launch_prep_model(ModelPx *model, int64_t begin, int64_t n, double c0, cudaStream_t s);
+// NEXT-3 background training (psfs_train_background): up to kMaxTrain frame
+// pointers travel in the kernel parameters (no device table, no sync).
+constexpr int kMaxTrain = 512;  // == PSFS_MAX_TRAIN_FRAMES
+struct TrainParams {
+    const uint8_t *frames[kMaxTrain];
+    int32_t n;
+    int64_t nelem;     // 3 * W * H
+    float floor_f;
+    float *mean, *sigma;
+    ModelPx *model;    // non-null: install (mu, sigma') into these records
+};
+cudaError_t launch_train(const TrainParams &p, cudaStream_t s);
 cudaError_t launch_voxel(const VParams &p, int F, cudaStream_t s, int *nblocks);
 int voxel_tiles(int xlen, int ylen, int k0, int k1, int ty, int kz);
 cudaError_t launch_surface(const uint32_t *bits, uint32_t *surf, int64_t *idx, int64_t capacity,

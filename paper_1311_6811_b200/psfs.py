@@ -38,7 +38,8 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_fast_rcp_enabled", "psfs_debug_rcp_check", "psfs_probe_l1_bandwidth",
            "psfs_set_stage1_path", "psfs_set_voxel_tile", "psfs_set_overlap",
            "psfs_set_carve", "psfs_surface", "psfs_smooth_threshold", "psfs_peer_alloc",
-           "psfs_peer_open", "psfs_reconstruct_peer", "psfs_peer_status", "psfs_color"]
+           "psfs_peer_open", "psfs_reconstruct_peer", "psfs_peer_status", "psfs_color",
+           "psfs_train_background"]
 
 
 class PsfsError(RuntimeError):
@@ -110,6 +111,7 @@ def lib():
         L.psfs_reconstruct_peer.argtypes = [vp, i32, vp, vp, vp]
         L.psfs_peer_status.argtypes = [vp, vp]
         L.psfs_color.argtypes = [vp, vp, vp, vp, C.c_int64, d, vp, vp, vp]
+        L.psfs_train_background.argtypes = [vp, i32, i32, vp, vp, vp, i32, vp]
         _lib = L
     return _lib
 
@@ -223,6 +225,28 @@ class Reconstructor:
         self._check(lib().psfs_set_background(self._h, int(cam), mean.shape[1], mean.shape[0],
                                               mean.ctypes.data, sigma.ctypes.data),
                     "psfs_set_background")
+
+    def train_background(self, cam, frames, install=True, outputs=True, stream=None):
+        """NEXT-3: train camera `cam`'s background model on the GPU from a uint8
+        CUDA tensor [n, H, W, 3] of background frames; install=True makes it the
+        camera's model.  Returns (mean, sigma) float32 CUDA tensors or None."""
+        import torch
+        if not (isinstance(frames, torch.Tensor) and frames.is_cuda and frames.dtype == torch.uint8
+                and frames.is_contiguous() and frames.dim() == 4):
+            raise TypeError("frames must be a contiguous uint8 CUDA tensor [n, H, W, 3]")
+        n = frames.shape[0]
+        per = frames[0].numel()
+        ptrs = _ptr_array([frames.data_ptr() + f * per for f in range(n)])
+        mean = sigma = None
+        if outputs:
+            mean = torch.empty(frames.shape[1:], dtype=torch.float32, device=frames.device)
+            sigma = torch.empty_like(mean)
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._check(lib().psfs_train_background(self._h, int(cam), int(n), ptrs,
+                                                _dev_ptr(mean, torch.float32),
+                                                _dev_ptr(sigma, torch.float32), int(bool(install)),
+                                                s), "psfs_train_background")
+        return mean, sigma
 
     def set_max_fuse(self, fmax: int):
         self._check(lib().psfs_set_max_fuse(self._h, int(fmax)), "psfs_set_max_fuse")
