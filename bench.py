@@ -596,7 +596,7 @@ def run_ours(args):
         us = device_us(lambda st: rec.smooth_threshold(Lf[0], smoothed=smv, bits=smb, stream=st), dev)
         smooth = {"us_per_frame": us,
                   "note": "NEXT-1 posterior 3x3x3 box filter + threshold (P:111, P:300), "
-                          "2 launches, not part of the headline step"}
+                          "2 launches (device time, CUDA-graph replay), not part of the headline step"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:

@@ -26,14 +26,22 @@ def _rec(scene="C1"):
     return s, from_scene(s)
 
 
-@pytest.mark.parametrize("n", [1, 7, 8, 33])
-def test_mean_sigma_parity(n):
+@pytest.mark.parametrize("n,misaligned", [(1, False), (7, False), (8, True), (33, False),
+                                         (33, True)])
+def test_mean_sigma_parity(n, misaligned):
+    """misaligned: frames at an odd address (the byte-load kernel variant)."""
     s, rec = _rec()
     rng = np.random.default_rng(n)
     H, W = int(s.heights[1]), int(s.widths[1])
     base = rng.integers(0, 256, (1, H, W, 3))
     fr = np.clip(base + rng.integers(-40, 41, (n, H, W, 3)), 0, 255).astype(np.uint8)
-    m, sg = rec.train_background(1, torch.from_numpy(fr).cuda(), install=False)
+    t = torch.from_numpy(fr).cuda()
+    if misaligned:
+        raw = torch.empty(t.numel() + 1, dtype=torch.uint8, device="cuda")
+        raw[1:].copy_(t.view(-1))
+        t = raw[1:].view(t.shape)
+        assert t.data_ptr() % 4 == 1
+    m, sg = rec.train_background(1, t, install=False)
     torch.cuda.synchronize()
     mo, so = oracle.train_background(list(fr), sigma_floor=1.0)
     assert np.allclose(m.cpu().numpy(), mo, rtol=1e-6, atol=0)
