@@ -54,6 +54,7 @@ def parse():
                          "3 four pixels/thread, 4 warp-row loads (A/B experiments)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-zslab", action="store_true", help="skip the C4 z-slab section")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true",
@@ -63,52 +64,88 @@ def parse():
 
 # ---------------------------------------------------------------- clocks
 
+_NVML_SAMPLER = r"""
+import sys, time
+import pynvml as N
+N.nvmlInit()
+h = N.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+        N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+while True:
+    sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+    r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+    print(f"{sm},{mx}," + ",".join("Active" if r & b else "Not Active" for b in bits), flush=True)
+    time.sleep(0.002)
+"""
+
+
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled every ~2 ms during the timed region by a
+    separate NVML process (no GIL contention with the launching thread; started
+    and confirmed running before the timed region).  Falls back to nvidia-smi."""
 
     def __init__(self, index=0):
         self.index = index
         self.proc = None
         self.lines = []
+        self.marks = []
 
     def start(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            self.proc = subprocess.Popen([sys.executable, "-c", _NVML_SAMPLER, str(self.index)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            first = self.proc.stdout.readline()  # blocks until NVML is up
+            if not first:
+                raise RuntimeError("nvml sampler failed")
+            self.lines.append(first.strip())
         except Exception:
-            self.proc = None
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                     "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            except Exception:
+                self.proc = None
+                return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def mark(self):
+        """Index of the next sample: call around the timed region."""
+        self.marks.append(len(self.lines))
+
     def stop(self):
         if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampler unavailable"]}
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
         except Exception:
             self.proc.kill()
         time.sleep(0.05)
+        lines = self.lines
+        if len(self.marks) >= 2 and self.marks[1] > self.marks[0]:
+            lines = lines[self.marks[0]:self.marks[1] + 1]  # samples inside the timed region
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
+            if len(parts) < 6:
                 continue
             try:
                 sm.append(float(parts[0]))
                 mx.append(float(parts[1]))
             except ValueError:
                 continue
-            for n, v in zip(names, parts[3:7]):
+            for n, v in zip(names, parts[2:6]):
                 if v.lower() == "active":
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None,
@@ -258,37 +295,47 @@ def device_us(fn, dev, reps=20):
     return e0.elapsed_time(e1) / reps * 1e3
 
 
-def zslab_bench(args, scene, frames_dev, rank, world, local, dev, stream,
-                variants=(("fused_peer", True), ("nccl_allgather", False))):
-    """z-slab partition: every rank owns zlen/N slices of the
-    grid and the full bitmask reaches every rank.  Each rank uses its own 16
-    frames (timing only; tests/test_gpu_peer.py checks the exchanged bits)."""
+def zslab_bench(args, scene, frames_dev, rank, world, local, dev, stream, variants=None):
+    """z-slab partition (BASELINE.json configs[3]): every rank
+    owns zlen/N slices of the grid, computes stage 1 over its band of rows and
+    stage 2 over its slab, and the full bitmask reaches every rank -- through
+    the fused peer exchange (stage 2 stores into every rank's buffer) or an
+    NCCL all-gather.  N = 1: one handle, nothing to exchange.  All ranks
+    reconstruct the same frames (the same seeded scene)."""
     import torch
     import torch.distributed as dist
     from paper_1311_6811_b200.parallel import ZSlabReconstructor
-    nf = 16
-    fr = frames_dev[:nf].contiguous()
-    out = {"frames_per_call": nf, "slices_per_rank": scene.grid.zlen // world}
+    if variants is None:
+        variants = ((("fused_peer", True), ("nccl_allgather", False)) if world > 1
+                    else (("single_gpu", False),))
+    nf = int(frames_dev.shape[0])
+    fr = frames_dev.contiguous()
+    g = scene.grid
+    out = {"frames_per_call": nf, "slices_per_rank": g.zlen // world, "world": world}
     for name, peer in variants:
         z = ZSlabReconstructor(scene, rank=rank, world=world, device=local, peer=peer,
                                max_frames=nf)
-        bits = None if peer else torch.zeros((nf, scene.grid.nwords), dtype=torch.int32, device=dev)
-        for _ in range(args.warmup):
+        bits = None if peer else torch.zeros((nf, g.nwords), dtype=torch.int32, device=dev)
+        for _ in range(2):
             z.reconstruct_batch(fr, nf, bits=bits, stream=stream)
         torch.cuda.synchronize(dev)
-        dist.barrier()
+        if world > 1:
+            dist.barrier()
+        reps = max(3, min(args.steps, 10))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(reps):
             z.reconstruct_batch(fr, nf, bits=bits, stream=stream)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         if peer:
             z.rec.peer_status(stream)
         t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item()) / args.steps
-        out[name] = {"ms_per_call": ms, "frames_per_s": nf / (ms / 1e3)}
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item()) / reps / nf
+        out[name] = {"ms_per_frame": ms, "frames_per_s": 1e3 / ms,
+                     "voxel_camera_projections_per_s": g.nvox * scene.ncam * 1e3 / ms}
         del z
     return out
 
@@ -352,7 +399,15 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     if sampler:
         sampler.start()
-        time.sleep(0.3)
+    # two more untimed steps: the GPU was idle while the sampler started
+    for k in range(2):
+        flush.fill_(k)
+        flush_sum = flush_rd.sum()
+        step(k)
+    torch.cuda.synchronize(dev)
+    rec.kernel_times(reset=True)
+    if sampler:
+        sampler.mark()
     launches = 0
     for k in range(args.steps):
         # L2 flush outside the step events: write a buffer larger than L2, then
@@ -365,6 +420,8 @@ def run_ours(args):
         ev[k][1].record(stream)
         launches += rec.last_launch_count
     torch.cuda.synchronize(dev)
+    if sampler:
+        sampler.mark()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
@@ -530,9 +587,15 @@ def run_ours(args):
     # ranks, 16 frames per call, with the bitmask exchange fused into stage 2
     # (peer stores + device barriers) and, for comparison, the NCCL all-gather
     zslab = None
-    if world > 1 and not args.profile:
+    if not args.profile and not args.no_zslab:
         try:
-            zslab = zslab_bench(args, scene, frames_dev, rank, world, local, dev, stream)
+            from synth.scene import make_frames, make_scene
+            zs = make_scene("C4")
+            zfr = torch.from_numpy(np.stack([make_frames(zs, f) for f in range(2)])).to(dev)
+            zslab = zslab_bench(args, zs, zfr, rank, world, local, dev, stream)
+            zslab["config"] = ("C4: 512^3 grid, 16 cameras at 1920x1080, z-slab partition over "
+                               f"{world} GPU(s), 2 frames per call")
+            del zfr
         except Exception as e:  # reported, never fatal for the headline
             zslab = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
 
@@ -550,6 +613,28 @@ def run_ours(args):
                    "note": "NEXT-2 inner-voxel removal (P:301): bit-parallel 6-neighbour test + ordered "
                            "compaction, 3 launches (device time, CUDA-graph replay), not part of the "
                            "headline step"}
+
+    # ---- secondary: one frame set per call (no batching: F = 1, latency view of
+    # the same C2 workload), L2 flushed before every call (outside the events)
+    single = None
+    if not args.profile:
+        _, B1 = rec.alloc_outputs(1, logodds=False)
+        for k in range(3):
+            rec.reconstruct(frames_dev[k], bits=B1, stream=stream)
+        torch.cuda.synchronize(dev)
+        tms = []
+        for k in range(args.steps):
+            flush.fill_(k)
+            flush_sum = flush_rd.sum()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rec.reconstruct(frames_dev[k % pool], bits=B1, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            tms.append(e0.elapsed_time(e1))
+        single = {"ms_per_frame": float(np.median(tms)), "frames_per_s": 1e3 / float(np.median(tms)),
+                  "note": "latency view: psfs_reconstruct of one frame set per call (no fusion), "
+                          "median over calls, L2 flushed before each"}
 
     # ---- secondary: NEXT-4 voxel colour (psfs_color) of one frame's surface voxels,
     # chained on the device after psfs_surface (count never read on the host)
@@ -623,10 +708,11 @@ def run_ours(args):
                                     if args.overlap >= 0 else "serial"),
                        "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the step events)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "carve": carve,
-            "surface": surface, "color": color, "smooth": smooth, "train": train, "zslab": zslab,
+            "single_frame": single, "surface": surface, "color": color, "smooth": smooth,
+            "train": train, "zslab": zslab,
             "gpu_launches": launches, "clocks": clocks,
             "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms),
-                        "max": max(step_ms)},
+                        "max": max(step_ms), "all": [round(x, 4) for x in step_ms]},
         }
         print(json.dumps(out), flush=True)
     if world > 1:

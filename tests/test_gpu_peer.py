@@ -117,6 +117,7 @@ def _bench_worker(rank, world, port, q):
         args = argparse.Namespace(steps=2, warmup=1)
         out = bench.zslab_bench(args, s, fr, rank, world, 0, torch.device("cuda", 0),
                                 torch.cuda.current_stream(), variants=(("fused_peer", True),))
+        assert out["world"] == world and out["frames_per_call"] == 16
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
