@@ -1,3 +1,19 @@
 mkdir -p gpurun_out
-python bench.py --no-e2e --no-cpu-baseline --no-zslab > gpurun_out/bench_steps.json 2>gpurun_out/bench_steps.err
-tail -1 gpurun_out/bench_steps.json | python -c "import json,sys; j=json.loads(sys.stdin.read()); print(j['value'], j['step_ms']['all'], j['clocks'])"
+: > gpurun_out/ab_summary.txt
+run() { # name lib extra-args
+  PSFS_LIB=$2 timeout 300 python bench.py --no-e2e --no-cpu-baseline --no-zslab $3 > gpurun_out/ab_$1.log 2>&1
+  python - "$1" >> gpurun_out/ab_summary.txt <<'PY'
+import json, sys
+n = sys.argv[1]
+try:
+    j = json.loads(open(f"gpurun_out/ab_{n}.log").read().strip().splitlines()[-1])
+    r = j["roofline"]; iso = r.get("isolated_serial") or {}
+    print(f"{n:24s} fps={j['value']:9.0f} med={j['step_ms']['median']*1e3:.1f}  vox={r['avg_launch_us']:6.1f} s1={r['other_kernel']['avg_launch_us']:6.1f} iso_s1={iso.get('k_likelihood',{}).get('avg_launch_us',0):6.1f} iso_vox={iso.get('k_voxel',{}).get('avg_launch_us',0):6.1f}")
+except Exception as e:
+    print(n, "FAILED", e)
+PY
+}
+run base paper_1311_6811_b200/libpsfs.so ""
+for v in s1na s1cs s1mna; do run $v variants/$v/libpsfs.so ""; done
+run base_b64 paper_1311_6811_b200/libpsfs.so "--batch 64 --pool 64"
+cat gpurun_out/ab_summary.txt

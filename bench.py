@@ -40,8 +40,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--batch", type=int, default=32, help="frames per step per GPU")
-    ap.add_argument("--pool", type=int, default=32, help="distinct frame sets cycled")
+    ap.add_argument("--batch", type=int, default=64, help="frames per step per GPU")
+    ap.add_argument("--pool", type=int, default=64, help="distinct frame sets cycled")
     ap.add_argument("--overlap", type=int, default=0,
                     help="overlap stage 1 of group g+1 with stage 2 of group g; value = k_voxel "
                          "blocks/SM cap (0: none); -1: serial schedule")
