@@ -13,7 +13,9 @@ except Exception as e:
     print(n, "FAILED", e)
 PY
 }
-run base paper_1311_6811_b200/libpsfs.so ""
-for v in s1na s1cs s1mna; do run $v variants/$v/libpsfs.so ""; done
-run base_b64 paper_1311_6811_b200/libpsfs.so "--batch 64 --pool 64"
+timeout 600 python -m pytest tests -q -m gpu -x -k "sixteen or batch_of_16 or overlapped or 64_frames" > gpurun_out/pytest_disc.log 2>&1; tail -4 gpurun_out/pytest_disc.log
+run disc paper_1311_6811_b200/libpsfs.so ""
+run nodisc variants/nodisc/libpsfs.so ""
+run disc2 paper_1311_6811_b200/libpsfs.so ""
+run nodisc2 variants/nodisc/libpsfs.so ""
 cat gpurun_out/ab_summary.txt

@@ -128,6 +128,25 @@ def test_c2_batch_of_16_paired_kernel():
     assert np.array_equal(g8["L"], g["L"])
 
 
+def test_c2_bench_launch_configuration_64_frames():
+    """bench.py's timed call: C2, 64 distinct frame sets in one
+    psfs_reconstruct_batch (four 16-frame passes, stage 1 of pass g+1
+    overlapped with stage 2 of pass g), every frame against the oracle."""
+    from paper_1311_6811_b200 import from_scene
+    s = make_scene("C2")
+    frames = [make_frames(s, f) for f in range(64)]
+    rec = from_scene(s)
+    rec.set_overlap(True, 0)
+    L, B = rec.alloc_outputs(64)
+    rec.reconstruct_batch(torch.from_numpy(np.stack(frames)).cuda(), 64, logodds=L, bits=B)
+    torch.cuda.synchronize()
+    assert rec.last_launch_count == 8
+    Lh, Bh = L.cpu().numpy(), B.cpu().numpy().view(np.uint32)
+    for f in range(64):
+        orc = oracle.scene_reconstruct(s, frames[f], nthreads=NTHREADS)
+        assert_parity(Lh[f], Bh[f], orc, s.grid.nvox)
+
+
 def test_batch_grouping_29_frames():
     """29 = 16 + 8 + 4 + 1 frames: every group size, against the oracle."""
     s = make_scene("C1")
