@@ -1,21 +1,9 @@
+# full GPU suite, default bench line, launch list, ncu --set full of both kernels
 mkdir -p gpurun_out
-: > gpurun_out/ab_summary.txt
-run() { # name lib extra-args
-  PSFS_LIB=$2 timeout 300 python bench.py --no-e2e --no-cpu-baseline --no-zslab $3 > gpurun_out/ab_$1.log 2>&1
-  python - "$1" >> gpurun_out/ab_summary.txt <<'PY'
-import json, sys
-n = sys.argv[1]
-try:
-    j = json.loads(open(f"gpurun_out/ab_{n}.log").read().strip().splitlines()[-1])
-    r = j["roofline"]; iso = r.get("isolated_serial") or {}
-    print(f"{n:24s} fps={j['value']:9.0f} med={j['step_ms']['median']*1e3:.1f}  vox={r['avg_launch_us']:6.1f} s1={r['other_kernel']['avg_launch_us']:6.1f} iso_s1={iso.get('k_likelihood',{}).get('avg_launch_us',0):6.1f} iso_vox={iso.get('k_voxel',{}).get('avg_launch_us',0):6.1f}")
-except Exception as e:
-    print(n, "FAILED", e)
-PY
-}
-timeout 600 python -m pytest tests -q -m gpu -x -k "sixteen or batch_of_16 or overlapped or 64_frames" > gpurun_out/pytest_disc.log 2>&1; tail -4 gpurun_out/pytest_disc.log
-run disc paper_1311_6811_b200/libpsfs.so ""
-run nodisc variants/nodisc/libpsfs.so ""
-run disc2 paper_1311_6811_b200/libpsfs.so ""
-run nodisc2 variants/nodisc/libpsfs.so ""
-cat gpurun_out/ab_summary.txt
+timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
+tail -1 gpurun_out/bench_default.json | python -c "import json,sys; j=json.loads(sys.stdin.read()); r=j['roofline']; print(j['value'], j['step_ms']['median'], r['avg_launch_us'], r['frac'], r['isolated_serial'], j['e2e']['value'], j['cpu_baseline']['value'], j['zslab'])"
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_r01.csv python bench.py --steps 3 --warmup 3 --profile --no-e2e --no-cpu-baseline --no-zslab > /dev/null 2>&1
+rm -f gpurun_out/prof_r01.ncu-rep
+timeout 600 ncu --set full --clock-control none --import-source on -k "regex:k_likelihood|k_voxel" -s 8 -c 2 -o gpurun_out/prof_r01 python bench.py --steps 3 --warmup 3 --profile --no-e2e --no-cpu-baseline --no-zslab --overlap -1 > /dev/null 2>&1
+ls -la gpurun_out/prof_r01.ncu-rep gpurun_out/launches_r01.csv
