@@ -525,10 +525,12 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": world * B * args.steps / (e_ms / 1e3), "unit": "frames/s",
-               "h2d_bytes_per_step": int(B * ncam * per_cam),
+               "h2d_bytes_per_step": int(B * 3 * ((roi[:, 1] - roi[:, 0]).astype(np.int64)
+                                                  * (roi[:, 3] - roi[:, 2])).sum()),
                "d2h_bytes_per_step": int(B * scene.grid.nwords * 4),
                "ms_per_step": e_ms / args.steps,
-               "how": "psfs_reconstruct_host: pinned host frames -> device staging (copy stream), "
+               "how": "psfs_reconstruct_host: pinned host frames (the region-of-interest rectangle "
+                      "of each image, 2-D copies) -> device staging (copy stream), "
                       "both stages, bitmask -> pinned host (second copy stream), double-buffered"}
 
     # ---- secondary: the two kernels in isolation (serial schedule), so their

@@ -165,7 +165,9 @@ int psfs_reconstruct_batch(psfs_handle *h, int32_t nframes, const uint8_t *const
  * several command queues): frames: HOST array of nframes*ncam HOST
  * pointers (page-locked memory gives real overlap), frame-major; logodds /
  * bits: nullable HOST outputs laid out as in psfs_reconstruct_batch.  The
- * library copies each group of frames into its own device staging buffers on
+ * library copies each group of frames -- only the region-of-interest rectangle
+ * of each image, the pixels stage 1 reads (psfs_debug_roi) -- into its own
+ * device staging buffers on
  * an internal copy stream, computes on cuda_stream, and copies the results back
  * on a second copy stream, double-buffered so group g+1's upload and group
  * g-1's download overlap group g's kernels.  Asynchronous: host outputs are
