@@ -1,4 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -q -m gpu -x -k "host" > gpurun_out/pytest_host.log 2>&1; tail -3 gpurun_out/pytest_host.log
-python bench.py --no-cpu-baseline --no-zslab > gpurun_out/bench_e2e.json 2>gpurun_out/bench_e2e.err
-tail -1 gpurun_out/bench_e2e.json | python -c "import json,sys; j=json.loads(sys.stdin.read()); print(j['value'], j['e2e'])"
+t0=$(date +%s); timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$? wall=$(( $(date +%s)-t0 ))s"; tail -2 gpurun_out/smoke.log
