@@ -446,8 +446,11 @@ def run_ours(args):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     hbm_src = ("of measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks
                else "of fallback 6.65 TB/s (B200_PROFILING.md)")
-    from paper_1311_6811_b200.psfs import probe_l1_bandwidth
+    from paper_1311_6811_b200.psfs import probe_gather_bandwidth, probe_l1_bandwidth
     l1_peak = probe_l1_bandwidth() / 1e9 if not args.profile else None
+    # k_voxel16's access pattern measured live: lane pairs on two-sector lines of a
+    # 64 MB L2-resident table, non-allocating 256-bit loads (psfs_probe_gather_bandwidth)
+    gather_peak = probe_gather_bandwidth(64 << 20) / 1e9 if not args.profile else None
     traffic = {}
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -492,6 +495,17 @@ def run_ours(args):
             "voxel_cam_frames_per_s": nvox * ncam * F / v_avg_s, "traffic": traffic.get("k_voxel"),
             "l1_load_probe_gbs": l1_peak},
     }
+    if F == 16 and gather_peak:
+        # the binding roofline of the 16-frame gather: the same access pattern's
+        # measured rate from L2 (the all-hit L1 line rate kept beside it)
+        kv = per_kernel["k_voxel"]
+        kv["all_hit_l1_line_bound"] = {"peak": kv["peak"], "frac": kv["achieved"] / kv["peak"],
+                                       "peak_source": kv["peak_source"]}
+        kv.update({"bound": "l2_gather", "peak": gather_peak,
+                   "peak_source": "measured live: psfs_probe_gather_bandwidth(64 MB) -- lane pairs "
+                                  "reading both 32-byte sectors of random 128-byte lines of an "
+                                  "L2-resident table with k_voxel16's non-allocating 256-bit load "
+                                  "and residency; DESIGN.md section 8"})
     for v in per_kernel.values():
         v["frac"] = v["achieved"] / v["peak"]
     dominant = "k_likelihood" if l_ms >= v_ms else "k_voxel"

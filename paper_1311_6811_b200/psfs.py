@@ -39,7 +39,7 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_set_stage1_path", "psfs_set_voxel_tile", "psfs_set_overlap",
            "psfs_set_carve", "psfs_surface", "psfs_smooth_threshold", "psfs_peer_alloc",
            "psfs_peer_open", "psfs_reconstruct_peer", "psfs_peer_status", "psfs_color",
-           "psfs_train_background"]
+           "psfs_train_background", "psfs_probe_gather_bandwidth"]
 
 
 class PsfsError(RuntimeError):
@@ -106,6 +106,7 @@ def lib():
         L.psfs_fast_rcp_enabled.argtypes = [vp]
         L.psfs_debug_rcp_check.argtypes = [C.c_float, C.c_float, C.POINTER(C.c_int64)]
         L.psfs_probe_l1_bandwidth.argtypes = [C.POINTER(C.c_double)]
+        L.psfs_probe_gather_bandwidth.argtypes = [C.c_int64, C.POINTER(C.c_double)]
         L.psfs_peer_alloc.argtypes = [vp, i32, C.POINTER(vp), vp]
         L.psfs_peer_open.argtypes = [vp, vp]
         L.psfs_reconstruct_peer.argtypes = [vp, i32, vp, vp, vp]
@@ -488,6 +489,15 @@ class Reconstructor:
     @property
     def last_launch_count(self):
         return int(lib().psfs_last_launch_count(self._h))
+
+
+def probe_gather_bandwidth(table_bytes: int = 64 << 20) -> float:
+    """Bytes/s of k_voxel16's gather pattern on the current device (psfs_probe_gather_bandwidth)."""
+    v = C.c_double()
+    rc = lib().psfs_probe_gather_bandwidth(int(table_bytes), C.byref(v))
+    if rc != PSFS_OK:
+        raise PsfsError(rc, "psfs_probe_gather_bandwidth")
+    return float(v.value)
 
 
 def debug_rcp_check(lo: float, hi: float) -> int:
