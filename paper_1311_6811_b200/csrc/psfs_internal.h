@@ -91,6 +91,12 @@ struct VParams {
     int32_t npeer;
     uint32_t *peer[kMaxPeers];
     int64_t peer_fstride;
+    // the same outputs as base + frame * stride (a lane-dependent frame index
+    // into bits[] / logodds[] would put those arrays in local memory)
+    uint32_t *bits_base;       // bits[0] (nullable)
+    int64_t bits_stride;       // words per frame
+    float *lo_base;            // logodds[0] (nullable)
+    int64_t lo_stride;         // floats per frame
 };
 
 // NEXT-4 voxel colour (psfs_color): per camera the pinned matrix, the image and
