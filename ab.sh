@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -q -m gpu -x -k "sixteen or batch_of_16 or 29_frames or ragged or general_priors or overlapped or carve or peer or 64_frames or tile" > gpurun_out/pytest_ep.log 2>&1; tail -3 gpurun_out/pytest_ep.log
+timeout 1500 python -m pytest tests -q -m gpu -x -k "sixteen or batch_of_16 or 29_frames or ragged or general_priors or overlapped or carve or peer or 64_frames or tile or zslab or full_size" > gpurun_out/pytest_st.log 2>&1; tail -3 gpurun_out/pytest_st.log
 : > gpurun_out/ab_summary.txt
 run() { # name lib extra-args
   PSFS_LIB=$2 timeout 300 python bench.py --no-e2e --no-cpu-baseline --no-zslab $3 > gpurun_out/ab_$1.log 2>&1
@@ -14,6 +14,6 @@ except Exception as e:
     print(n, "FAILED", e)
 PY
 }
-run ep paper_1311_6811_b200/libpsfs.so ""
-run ep_f8 paper_1311_6811_b200/libpsfs.so "--fuse 8"
+run stage paper_1311_6811_b200/libpsfs.so ""
+run stage2 paper_1311_6811_b200/libpsfs.so ""
 cat gpurun_out/ab_summary.txt

@@ -97,6 +97,7 @@ struct VParams {
     int64_t bits_stride;       // words per frame
     float *lo_base;            // logodds[0] (nullable)
     int64_t lo_stride;         // floats per frame
+    int32_t word_rows;         // xlen % 32 == 0: a 32-wide tile row is one bitmask word
 };
 
 // NEXT-4 voxel colour (psfs_color): per camera the pinned matrix, the image and
