@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-python bench.py --no-e2e --no-cpu-baseline > gpurun_out/bench_z.json 2>gpurun_out/bench_z.err
-tail -1 gpurun_out/bench_z.json | python -c "import json,sys; j=json.loads(sys.stdin.read()); print(j['value'], j['zslab'])"; tail -2 gpurun_out/bench_z.err
+timeout 1500 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "sixteen_frame_pass" > gpurun_out/pytest_fs.log 2>&1; tail -3 gpurun_out/pytest_fs.log

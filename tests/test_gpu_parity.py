@@ -310,3 +310,36 @@ def test_full_size_sampled(name):
     shifts = torch.arange(32, device="cuda", dtype=torch.int32)
     allbits = ((B[0].view(-1, 1) >> shifts) & 1).view(-1)[: s.grid.nvox].bool()
     assert not bool((allbits & (L[0] < 0)).any()) and not bool((~allbits & (L[0] > 0)).any())
+
+
+@pytest.mark.parametrize("name,with_logodds", [("C4", True), ("C5", False)])
+def test_full_size_sixteen_frame_pass(name, with_logodds):
+    """The full-size configurations in bench.py's launch configuration: one
+    16-frame pass (k_voxel16, NCAM = 16 for C4, the generic camera loop for
+    C5's 32 cameras) over 2 distinct frame sets repeated 8 times; both distinct
+    frames checked on the voxel sample against the oracle (log-odds for C4,
+    bits for C5, whose 16 log-odds volumes would need 64 GB), and every repeat
+    bit-identical to its original."""
+    from paper_1311_6811_b200 import from_scene
+    s = make_scene(name)
+    two = [make_frames(s, 0), make_frames(s, 1)]
+    fr = torch.from_numpy(np.stack(two)).cuda().repeat(8, 1, 1, 1, 1)
+    rec = from_scene(s)
+    L, B = rec.alloc_outputs(16, logodds=with_logodds)
+    rec.reconstruct_batch(fr, 16, logodds=L, bits=B)
+    torch.cuda.synchronize()
+    for f in range(2, 16):
+        assert torch.equal(B[f], B[f % 2])
+    rng = np.random.default_rng(11)
+    vox = _sample_voxels(s.grid, rng)
+    vt = torch.from_numpy(vox).cuda()
+    for f in range(2):
+        Lo, post = oracle.fuse_sample(s.P, s.widths, s.heights, s.grid, two[f], s.mu, s.sigma, vox,
+                                      nthreads=NTHREADS)
+        if with_logodds:
+            assert np.abs(L[f][vt].cpu().numpy().astype(np.float64) - Lo).max() <= 1e-4
+        words = B[f][(vt >> 5)].cpu().numpy().view(np.uint32)
+        bits = ((words >> (vox & 31).astype(np.uint32)) & 1).astype(bool)
+        mism = bits != (post > 0.5)
+        assert not (mism & ~(np.abs(post - 0.5) < 1e-4)).any()
+        assert bits.sum() > 0
