@@ -243,6 +243,46 @@ int psfs_set_stage1_path(psfs_handle *h, int32_t path);
  * identical to the full sum's.  Ignored when log-odds are requested. */
 int psfs_set_carve(psfs_handle *h, int32_t enabled);
 
+/* Coarse passes for bits-only calls (the threshold of
+ * P:111 / R#14 needs only the sign of L - logit tau).  When a reconstruct call
+ * requests no log-odds, stage 1 stores an 8-bit code per pixel and frame that
+ * brackets the exact Q11.20 term q of Eq 5-9 (c 2^sh <= q <= c 2^sh + wc), 32
+ * frames per 32-byte record; stage 2 sums the codes of every voxel's cameras
+ * and decides every voxel-frame whose bracket lies on one side of T_q; the
+ * others (rare: |L - logit tau| within about ncam * 2^(sh-20)) are summed
+ * exactly from the frames and the model with the exact path's per-pixel
+ * arithmetic.  The bitmask is bit-identical to the exact path's.
+ * The undecided voxel-frames of a pass are listed by k_voxel_c8 and summed by a
+ * second kernel (k_fixup_c8, one warp per entry, cameras across the lanes) that
+ * patches their bits; entries beyond the list's capacity are summed in place by
+ * the voxel kernel (slow, still exact).
+ * mode: 0 = off (always the exact int32 path), 1 = on (default), 2 = test mode
+ * (every voxel-frame resolved exactly through the fix-up).  max_frames: frames
+ * per coarse pass, 1..32 (default 32).  fix_capacity: list entries (8 bytes
+ * each), 0 = default 2^20.  Coarse passes apply when the params
+ * admit them (psfs_coarse_plan), xlen % 32 == 0, the tile depth kz <= 8 and
+ * carve is off; otherwise calls take the exact path. */
+int psfs_set_coarse(psfs_handle *h, int32_t mode, int32_t max_frames, int64_t fix_capacity);
+
+/* Host-only: the coarse-code plan for params and ncam cameras.  out (HOST, 4
+ * int32): admitted (sigma_floor >= 0.25 and p_O in [1e-3, 1 - 1e-3]), sh (code
+ * quantum 2^sh in Q11.20 units), bias (the code of t = 0), wc (bracket width:
+ * q in [c 2^sh, c 2^sh + wc]); eps (nullable): the FP32 error bound in t the
+ * bracket is widened by. */
+int psfs_coarse_plan(const psfs_params *params, int32_t ncam, int32_t *out, double *eps);
+
+/* applies (nullable): whether a bits-only call of this handle takes coarse
+ * passes; fixups (nullable): voxel-frames resolved exactly since the last reset
+ * (synchronous read of a device counter); reset != 0 zeroes the counter. */
+int psfs_coarse_status(psfs_handle *h, int32_t *applies, int64_t *fixups, int32_t reset);
+
+/* Coarse stage 1 for one frame set over whole images: the code byte (c + bias)
+ * of every pixel, cameras concatenated (DEVICE out, sum_c W_c*H_c bytes), for
+ * checking the bracket against psfs_debug_terms.  Asynchronous on cuda_stream.
+ * PSFS_ESTATE when the params admit no coarse codes. */
+int psfs_debug_codes(psfs_handle *h, const uint8_t *const *frames, uint8_t *codes_out,
+                     void *cuda_stream);
+
 /* Overlapped batches (default on): with more than one frame group in a
  * psfs_reconstruct_batch call, stage 1 of group g+1 runs on an internal stream
  * beside stage 2 of group g (two term buffers); voxel_blocks_per_sm > 0 caps

@@ -100,6 +100,67 @@ struct VParams {
     int32_t word_rows;         // xlen % 32 == 0: a 32-wide tile row is one bitmask word
 };
 
+// ---- coarse passes (bits-only calls) -------------------
+// Stage 1 stores, per pixel and frame, an 8-bit code c + bias of the Q11.20 term
+// q with c 2^sh <= q <= c 2^sh + wc (c from an FP32 evaluation of t, widened by
+// its error bound); the 32 frames of a pass share one 32-byte record.  Stage 2
+// sums codes, decides every voxel-frame whose bounds lie on one side of T_q, and
+// recomputes the rest exactly (the same per-pixel arithmetic as k_likelihood).
+constexpr int kMaxFC = 32;  // frames per coarse pass (one byte each per record)
+
+struct S1CParams {
+    S1Cam cam[kMaxCam];                      // ROI, model / code offsets (tstride = row stride)
+    const uint8_t *frames[kMaxFC][kMaxCam];  // [f][c], f < nf
+    const struct ModelPx *model;
+    uint8_t *codes;      // (toff + p) * rec + f
+    int32_t rec;         // bytes per code record: 32 (passes) or 1 (debug, nf = 1)
+    int32_t ncam, nf;    // frames in this pass (1..32)
+    int32_t quarters;    // ceil(nf / 8): 8-frame parts in adjacent blocks
+    double lr;           // ln(1 - p_O) - ln p_O
+    float s;             // 2^(20 - sh)
+    float zoff;          // (-ln p_O - eps) s + bias
+};
+
+struct VCCam {
+    float A[12];    // pinned matrix (as VCam)
+    int32_t W, H;
+    uint32_t toff;  // padded code image offset (pixels)
+    uint32_t Wp;    // W + 1
+    int64_t off;    // model record offset (fix-up)
+};
+
+struct VCParams {
+    VCCam cam[kMaxCam];
+    const uint8_t *frames[kMaxFC][kMaxCam];  // fix-up: the exact terms are recomputed
+    const struct ModelPx *model;
+    const uint8_t *codes;     // 32-byte records
+    uint32_t K0, K1;          // packed 16-bit thresholds: field >= K1 -> bit 1; K0 <= field < K1 -> exact
+    int32_t Tq;
+    int32_t ncam, nf;
+    int32_t xlen, ylen, k0, k1;
+    int32_t fast_rcp;
+    double dlo, lnpo;         // exact path constants (k_likelihood): (ln(1-p_O) - ln p_O) 2^20, ln p_O 2^20
+    unsigned long long *tile_counter;
+    long long tile_base;
+    int32_t ntiles, kz;
+    uint32_t *bits_base;      // frame f at bits_base + f * bits_stride (nullable when npeer > 0)
+    int64_t bits_stride;
+    int32_t npeer;
+    uint32_t *peer[kMaxPeers];
+    int64_t peer_fstride;
+    unsigned long long *fix_count;  // nullable: voxel-frames resolved exactly
+    // undecided voxel-frames: (v << 5 | frame) appended at fix_list[*fix_head], then
+    // k_fixup_c8 sums them exactly and patches the bits; beyond fix_cap the lane
+    // resolves them in place (slow, correct)
+    unsigned long long *fix_list;
+    unsigned long long *fix_head;  // [0] entries, [1] k_fixup_c8 blocks done (reset by its last block)
+    uint64_t fix_cap;
+};
+
+cudaError_t launch_likelihood_coarse(const S1CParams &p, int max_roi_px, cudaStream_t s);
+cudaError_t launch_voxel_coarse(const VCParams &p, cudaStream_t s, int *nblocks);
+cudaError_t launch_fixup_coarse(const VCParams &p, cudaStream_t s);
+
 // NEXT-4 voxel colour (psfs_color): per camera the pinned matrix, the image and
 // the model records of its pixels.
 struct ColorCam {

@@ -39,7 +39,9 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_set_stage1_path", "psfs_set_voxel_tile", "psfs_set_overlap",
            "psfs_set_carve", "psfs_surface", "psfs_smooth_threshold", "psfs_peer_alloc",
            "psfs_peer_open", "psfs_reconstruct_peer", "psfs_peer_status", "psfs_color",
-           "psfs_train_background", "psfs_probe_gather_bandwidth"]
+           "psfs_train_background", "psfs_probe_gather_bandwidth", "psfs_set_coarse",
+           "psfs_coarse_plan", "psfs_coarse_status", "psfs_debug_codes"]
+MAX_COARSE = 32
 
 
 class PsfsError(RuntimeError):
@@ -113,6 +115,10 @@ def lib():
         L.psfs_peer_status.argtypes = [vp, vp]
         L.psfs_color.argtypes = [vp, vp, vp, vp, C.c_int64, d, vp, vp, vp]
         L.psfs_train_background.argtypes = [vp, i32, i32, vp, vp, vp, i32, vp]
+        L.psfs_set_coarse.argtypes = [vp, i32, i32, C.c_int64]
+        L.psfs_coarse_plan.argtypes = [C.POINTER(Params), i32, vp, C.POINTER(d)]
+        L.psfs_coarse_status.argtypes = [vp, C.POINTER(i32), C.POINTER(C.c_int64), i32]
+        L.psfs_debug_codes.argtypes = [vp, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -122,6 +128,20 @@ def default_params() -> dict:
     lib().psfs_default_params(C.byref(p))
     return dict(occlusion_prior=p.occlusion_prior, voxel_prior=p.voxel_prior,
                 threshold=p.threshold, sigma_floor=p.sigma_floor)
+
+
+def coarse_plan(params: dict | None = None, ncam: int = 8) -> dict:
+    """Host-only psfs_coarse_plan: the code bracket for these params."""
+    p = Params()
+    lib().psfs_default_params(C.byref(p))
+    for k, v in (params or {}).items():
+        setattr(p, k, float(v))
+    out = np.zeros(4, np.int32)
+    eps = C.c_double()
+    rc = lib().psfs_coarse_plan(C.byref(p), int(ncam), out.ctypes.data, C.byref(eps))
+    if rc != PSFS_OK:
+        raise PsfsError(rc, "psfs_coarse_plan")
+    return dict(ok=bool(out[0]), sh=int(out[1]), bias=int(out[2]), wc=int(out[3]), eps=eps.value)
 
 
 def _ptr_array(ptrs):
@@ -251,6 +271,20 @@ class Reconstructor:
 
     def set_max_fuse(self, fmax: int):
         self._check(lib().psfs_set_max_fuse(self._h, int(fmax)), "psfs_set_max_fuse")
+
+    def set_coarse(self, mode: int = 1, max_frames: int = MAX_COARSE, fix_capacity: int = 0):
+        """Coarse passes for bits-only calls: 0 off, 1 on (default), 2 every
+        voxel-frame resolved exactly (test mode); frames per pass 1..32;
+        fix-up list entries (0 = default 2^20)."""
+        self._check(lib().psfs_set_coarse(self._h, int(mode), int(max_frames), int(fix_capacity)),
+                    "psfs_set_coarse")
+
+    def coarse_status(self, reset: bool = False):
+        """(applies to bits-only calls, voxel-frames resolved exactly since the last reset)."""
+        a, n = C.c_int32(), C.c_int64()
+        self._check(lib().psfs_coarse_status(self._h, C.byref(a), C.byref(n), int(bool(reset))),
+                    "psfs_coarse_status")
+        return bool(a.value), int(n.value)
 
     def set_carve(self, on: bool):
         """Bits-only early exit (exact bitmask; ignored when log-odds are requested)."""
@@ -437,6 +471,15 @@ class Reconstructor:
         fp = self._frame_ptrs(frames, 1)
         s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
         self._check(lib().psfs_debug_terms(self._h, fp, out.data_ptr(), s), "psfs_debug_terms")
+        return out
+
+    def debug_codes(self, frames, stream=None):
+        """Coarse stage 1 of one frame set over whole images: uint8 codes (c + bias)."""
+        import torch
+        out = torch.empty(self.npix, dtype=torch.uint8, device=torch.device("cuda", self.device))
+        fp = self._frame_ptrs(frames, 1)
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._check(lib().psfs_debug_codes(self._h, fp, out.data_ptr(), s), "psfs_debug_codes")
         return out
 
     def matrices(self):
