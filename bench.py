@@ -45,7 +45,10 @@ def parse():
     ap.add_argument("--overlap", type=int, default=0,
                     help="overlap stage 1 of group g+1 with stage 2 of group g; value = k_voxel "
                          "blocks/SM cap (0: none); -1: serial schedule")
-    ap.add_argument("--fuse", type=int, default=16, help="frames fused per kernel pass")
+    ap.add_argument("--fuse", type=int, default=16, help="frames fused per exact-path pass")
+    ap.add_argument("--coarse", type=int, default=1, choices=[0, 1],
+                    help="coarse passes for the bits-only headline (psfs_set_coarse; 0: exact path)")
+    ap.add_argument("--coarse-frames", type=int, default=32, help="frames per coarse pass")
     ap.add_argument("--config", default="C2")
     ap.add_argument("--ty", type=int, default=1)
     ap.add_argument("--kz", type=int, default=4)
@@ -367,6 +370,8 @@ def run_ours(args):
     rec.set_stage1_path(args.stage1)
     rec.set_voxel_tile(args.ty, args.kz)
     rec.set_overlap(args.overlap >= 0, max(args.overlap, 0))
+    rec.set_coarse(args.coarse, args.coarse_frames)
+    coarse = rec.coarse_status()[0]
     frames_dev = torch.from_numpy(frames).to(dev)
     L, Bits = rec.alloc_outputs(B, logodds=False, bits=True)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
@@ -406,6 +411,7 @@ def run_ours(args):
         step(k)
     torch.cuda.synchronize(dev)
     rec.kernel_times(reset=True)
+    rec.coarse_status(reset=True)
     if sampler:
         sampler.mark()
     launches = 0
@@ -428,6 +434,7 @@ def run_ours(args):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
     kt = rec.kernel_times(reset=True)
+    fixups = rec.coarse_status(reset=True)[1]
     rec.set_profiling(False)
     if world > 1:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
@@ -450,7 +457,10 @@ def run_ours(args):
     l1_peak = probe_l1_bandwidth() / 1e9 if not args.profile else None
     # k_voxel16's access pattern measured live: lane pairs on two-sector lines of a
     # 64 MB L2-resident table, non-allocating 256-bit loads (psfs_probe_gather_bandwidth)
-    gather_peak = probe_gather_bandwidth(64 << 20) / 1e9 if not args.profile else None
+    if coarse:  # k_voxel_c8: one 32-byte sector per lane, 2 blocks/SM, a ~32 MB code table
+        gather_peak = probe_gather_bandwidth(32 << 20, 1, 2) / 1e9 if not args.profile else None
+    else:
+        gather_peak = probe_gather_bandwidth(64 << 20, 2, 3) / 1e9 if not args.profile else None
     traffic = {}
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -459,13 +469,14 @@ def run_ours(args):
         pass
     roi = rec.roi()
     roi_px = int(((roi[:, 1] - roi[:, 0]).astype(np.int64) * (roi[:, 3] - roi[:, 2])).sum())
-    F = args.fuse
+    F = args.coarse_frames if coarse else args.fuse
     l_ms, l_n = kt["k_likelihood"]
     v_ms, v_n = kt["k_voxel"]
     # stage 1 algorithmic bytes per launch (F frames fused): the model as
     # given (mu, sigma: 24 B/px) once, image 3 B/px and term 4 B/px per frame, over
     # the planned pixel rectangle
-    s1_bytes = roi_px * (24 + 7 * F)
+    # (coarse passes: 1-byte codes instead of 4-byte terms)
+    s1_bytes = roi_px * (24 + (4 if coarse else 7) * F)
     s1_avg_s = (l_ms / max(l_n, 1)) / 1e3
     # stage 2: the gather is bound by the L1TEX data pipe, one line-wavefront per
     # clock per SM (ncu: l1tex__data_pipe_lsu_wavefronts); algorithmic wavefronts =
@@ -473,18 +484,20 @@ def run_ours(args):
     # carrying wf_bytes useful bytes (32: one sector, F = 8; 64: two sectors of
     # one line, F = 16); peak = 1 wavefront/clk/SM x wf_bytes
     v_avg_s = (v_ms / max(v_n, 1)) / 1e3
-    sectors, wf_bytes = gather_sectors(scene, F)
+    sectors, wf_bytes = gather_sectors(scene, 8 if coarse else F)  # coarse: 32-B records, one per lane
     s2_bytes = sectors * wf_bytes
     sm_clk = (clocks or {}).get("sm_mhz") or float(peaks.get("sm_max_mhz", 1965.0))
     import torch as _t
     nsm = _t.cuda.get_device_properties(dev).multi_processor_count
     l1_sector_peak = nsm * sm_clk * 1e6 * wf_bytes / 1e9
+    s1_name = "k_likelihood_c8" if coarse else "k_likelihood"
+    s2_name = "k_voxel_c8 + k_fixup_c8" if coarse else ("k_voxel16" if F == 16 else "k_voxel")
     per_kernel = {
-        "k_likelihood": {
+        "k_likelihood": {"name": s1_name,
             "bound": "hbm", "achieved": s1_bytes / s1_avg_s / 1e9, "peak": hbm_peak,
             "unit": "GB/s", "peak_source": hbm_src, "algorithmic_bytes_per_launch": s1_bytes,
             "avg_launch_us": s1_avg_s * 1e6, "traffic": traffic.get("k_likelihood")},
-        "k_voxel": {
+        "k_voxel": {"name": s2_name,
             "bound": "l1", "achieved": s2_bytes / v_avg_s / 1e9, "peak": l1_sector_peak,
             "unit": "GB/s",
             "peak_source": f"derived: {nsm} SMs x 1 L1TEX data-pipe wavefront/clk x {wf_bytes} "
@@ -495,7 +508,18 @@ def run_ours(args):
             "voxel_cam_frames_per_s": nvox * ncam * F / v_avg_s, "traffic": traffic.get("k_voxel"),
             "l1_load_probe_gbs": l1_peak},
     }
-    if F == 16 and gather_peak:
+    if coarse and gather_peak:
+        kv = per_kernel["k_voxel"]
+        kv["all_hit_l1_line_bound"] = {"peak": kv["peak"], "frac": kv["achieved"] / kv["peak"],
+                                       "peak_source": kv["peak_source"]}
+        kv.update({"bound": "l2_gather", "peak": gather_peak,
+                   "fixups_per_step": fixups / max(args.steps, 1),
+                   "peak_source": "measured live: psfs_probe_gather_bandwidth(32 MB, 1 sector/line, "
+                                  "2 blocks/SM) -- every lane reads one 32-byte sector of its own "
+                                  "random 128-byte line of an L2-resident table with k_voxel_c8's "
+                                  "non-allocating 256-bit load and residency; the timed launch "
+                                  "includes k_fixup_c8; DESIGN.md section 8"})
+    elif F == 16 and gather_peak:
         # the binding roofline of the 16-frame gather: the same access pattern's
         # measured rate from L2 (the all-hit L1 line rate kept beside it)
         kv = per_kernel["k_voxel"]
@@ -511,9 +535,10 @@ def run_ours(args):
     dominant = "k_likelihood" if l_ms >= v_ms else "k_voxel"
     other = "k_voxel" if dominant == "k_likelihood" else "k_likelihood"
     share = {"k_likelihood": l_ms / max(l_ms + v_ms, 1e-12), "k_voxel": v_ms / max(l_ms + v_ms, 1e-12)}
-    roofline = dict(kernel=dominant, **per_kernel[dominant])
-    roofline["kernel_share"] = share
-    roofline["other_kernel"] = dict(kernel=other, **per_kernel[other])
+    roofline = dict(kernel=per_kernel[dominant].pop("name"), **per_kernel[dominant])
+    roofline["kernel_share"] = {per_kernel[k].get("name", k) if k != dominant else roofline["kernel"]: v
+                                for k, v in share.items()}
+    roofline["other_kernel"] = dict(kernel=per_kernel[other].pop("name"), **per_kernel[other])
 
     # ---- end to end through the C ABI with HOST buffers (pinned), per step:
     # H2D of the batch's frames, both stages, D2H of the bitmask
@@ -598,6 +623,34 @@ def run_ours(args):
                  "ms_per_step": cms / args.steps,
                  "note": "bits-only early exit (psfs_set_carve): a warp stops adding cameras once "
                          "its voxels are provably unoccupied; bitmask identical; not the headline"}
+
+    # ---- secondary: the exact int32 path for the same bits-only step (coarse off);
+    # the bitmask is identical (tests/test_gpu_coarse.py)
+    exact = None
+    if not args.profile and coarse:
+        rec.set_coarse(0, args.coarse_frames)
+        for k in range(2):
+            step(k)
+        torch.cuda.synchronize(dev)
+        xms = 0.0
+        for k in range(args.steps):
+            flush.fill_(k)
+            flush_sum = flush_rd.sum()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step(args.warmup + k)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            xms += e0.elapsed_time(e1)
+        rec.set_coarse(args.coarse, args.coarse_frames)
+        if world > 1:
+            t = torch.tensor([xms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            xms = float(t.item())
+        exact = {"value": world * B * args.steps / (xms / 1e3), "unit": "frames/s",
+                 "ms_per_step": xms / args.steps,
+                 "note": f"the exact int32 path (k_likelihood + k_voxel16, {args.fuse}-frame passes) "
+                         "for the same bits-only step; identical bitmask; not the headline"}
 
     # ---- secondary (N > 1 only): z-slab partition of the same grid across the
     # ranks, 16 frames per call, with the bitmask exchange fused into stage 2
@@ -714,10 +767,13 @@ def run_ours(args):
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64+f32+i32", "data": "synthetic",
+            "dtype": ("f32+u8+i32 (coarse codes; f64 exact fix-up)" if coarse else "f64+f32+i32"),
+            "data": "synthetic",
             "voxel_camera_projections_per_s": fps * nvox * ncam,
             "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}",
                        "frames_per_step_per_gpu": B, "fused_frames_per_pass": F,
+                       "path": ("coarse passes (8-bit bracketing codes, exact fix-up; bitmask "
+                                "identical to the exact path)" if coarse else "exact int32 terms"),
                        "grid": [scene.grid.xlen, scene.grid.ylen, scene.grid.zlen],
                        "cameras": ncam, "image": [int(scene.widths[0]), int(scene.heights[0])],
                        "distinct_frame_sets": pool, "parallelism": f"frame-parallel x{world}",
@@ -725,7 +781,7 @@ def run_ours(args):
                                     + (f" (k_voxel capped at {args.overlap} blocks/SM)" if args.overlap > 0 else "")
                                     if args.overlap >= 0 else "serial"),
                        "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the step events)"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "carve": carve,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "carve": carve, "exact_path": exact,
             "single_frame": single, "surface": surface, "color": color, "smooth": smooth,
             "train": train, "zslab": zslab,
             "gpu_launches": launches, "clocks": clocks,

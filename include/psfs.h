@@ -370,12 +370,16 @@ int psfs_fast_rcp_enabled(const psfs_handle *h);
  * gather is compared against. */
 int psfs_probe_l1_bandwidth(double *bytes_per_s);
 
-/* Microbenchmark on the current device: bytes/s delivered by k_voxel16's
- * gather pattern -- lane pairs reading the two 32-byte sectors of random
- * 128-byte lines of a table of table_bytes (L2-resident when below ~100 MB)
- * with the same non-allocating 256-bit load, k_voxel16's residency of 3 x 256
- * threads per SM -- the measured peak of its roofline. */
-int psfs_probe_gather_bandwidth(int64_t table_bytes, double *bytes_per_s);
+/* Microbenchmark on the current device: bytes/s delivered by a voxel kernel's
+ * gather pattern over random 128-byte lines of a table of table_bytes
+ * (L2-resident when below ~100 MB), non-allocating 256-bit loads, at
+ * blocks_per_sm x 256 threads per SM (1..8): sectors_per_line = 2 is
+ * k_voxel16's (lane pairs read the two 32-byte sectors of one line, 3 blocks
+ * per SM), 1 is k_voxel_c8's (each lane one 32-byte sector of its own line, 2
+ * blocks per SM) -- the measured peaks of their rooflines.
+ * Errors: PSFS_EINVAL, PSFS_ENOMEM, PSFS_ECUDA. */
+int psfs_probe_gather_bandwidth(int64_t table_bytes, int32_t sectors_per_line, int32_t blocks_per_sm,
+                                double *bytes_per_s);
 
 /* Test hook: on the current device, count the floats w in [lo, hi) (every bit
  * pattern) whose fast reciprocal differs from the IEEE RN(1/w).  lo > 0. */

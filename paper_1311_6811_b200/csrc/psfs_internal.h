@@ -218,7 +218,7 @@ cudaError_t launch_smooth(const float *logodds, float *P, float *smoothed, uint3
                           int ylen, int zlen, float tau, cudaStream_t s);
 cudaError_t launch_peer_barrier(const PeerBarrier &b, cudaStream_t s);
 cudaError_t launch_color(const ColorParams &p, cudaStream_t s);
-cudaError_t launch_gather_probe(const void *tab, uint32_t lines_mask, int blocks, int iters, int *out,
+cudaError_t launch_gather_probe(const void *tab, uint32_t lines_mask, int blocks, int iters, int G, int *out,
                                 cudaStream_t s);
 cudaError_t launch_l1_probe(const void *buf, int blocks, int iters, int *out, cudaStream_t s);
 cudaError_t launch_rcp_check(uint32_t lo_bits, uint32_t hi_bits, unsigned long long *bad,

@@ -108,7 +108,7 @@ def lib():
         L.psfs_fast_rcp_enabled.argtypes = [vp]
         L.psfs_debug_rcp_check.argtypes = [C.c_float, C.c_float, C.POINTER(C.c_int64)]
         L.psfs_probe_l1_bandwidth.argtypes = [C.POINTER(C.c_double)]
-        L.psfs_probe_gather_bandwidth.argtypes = [C.c_int64, C.POINTER(C.c_double)]
+        L.psfs_probe_gather_bandwidth.argtypes = [C.c_int64, i32, i32, C.POINTER(C.c_double)]
         L.psfs_peer_alloc.argtypes = [vp, i32, C.POINTER(vp), vp]
         L.psfs_peer_open.argtypes = [vp, vp]
         L.psfs_reconstruct_peer.argtypes = [vp, i32, vp, vp, vp]
@@ -534,10 +534,14 @@ class Reconstructor:
         return int(lib().psfs_last_launch_count(self._h))
 
 
-def probe_gather_bandwidth(table_bytes: int = 64 << 20) -> float:
-    """Bytes/s of k_voxel16's gather pattern on the current device (psfs_probe_gather_bandwidth)."""
+def probe_gather_bandwidth(table_bytes: int = 64 << 20, sectors_per_line: int = 2,
+                           blocks_per_sm: int = 3) -> float:
+    """Bytes/s of a voxel kernel's gather pattern on the current device
+    (psfs_probe_gather_bandwidth): sectors_per_line 2 = k_voxel16 (lane pairs on
+    two-sector records, 3 blocks/SM), 1 = k_voxel_c8 (one sector per lane, 2 blocks/SM)."""
     v = C.c_double()
-    rc = lib().psfs_probe_gather_bandwidth(int(table_bytes), C.byref(v))
+    rc = lib().psfs_probe_gather_bandwidth(int(table_bytes), int(sectors_per_line), int(blocks_per_sm),
+                                           C.byref(v))
     if rc != PSFS_OK:
         raise PsfsError(rc, "psfs_probe_gather_bandwidth")
     return float(v.value)
