@@ -258,11 +258,14 @@ int psfs_set_carve(psfs_handle *h, int32_t enabled);
  * the voxel kernel (slow, still exact).
  * mode: 0 = off (always the exact int32 path), 1 = on (default), 2 = test mode
  * (every voxel-frame resolved exactly through the fix-up).  max_frames: frames
- * per coarse pass, 1..32 (default 32).  fix_capacity: list entries (8 bytes
- * each), 0 = default 2^20.  Coarse passes apply when the params
+ * per coarse pass, 1..32 (default 32; a call's frames are split into balanced
+ * passes).  min_frames: calls with fewer frames take the exact path, which is
+ * faster for small batches (0 = default 16).  fix_capacity: list entries (8
+ * bytes each), 0 = default 2^20.  Coarse passes apply when the params
  * admit them (psfs_coarse_plan), xlen % 32 == 0, the tile depth kz <= 8 and
  * carve is off; otherwise calls take the exact path. */
-int psfs_set_coarse(psfs_handle *h, int32_t mode, int32_t max_frames, int64_t fix_capacity);
+int psfs_set_coarse(psfs_handle *h, int32_t mode, int32_t max_frames, int32_t min_frames,
+                    int64_t fix_capacity);
 
 /* Host-only: the coarse-code plan for params and ncam cameras.  out (HOST, 4
  * int32): admitted (sigma_floor >= 0.25 and p_O in [1e-3, 1 - 1e-3]), sh (code
@@ -271,8 +274,8 @@ int psfs_set_coarse(psfs_handle *h, int32_t mode, int32_t max_frames, int64_t fi
  * bracket is widened by. */
 int psfs_coarse_plan(const psfs_params *params, int32_t ncam, int32_t *out, double *eps);
 
-/* applies (nullable): whether a bits-only call of this handle takes coarse
- * passes; fixups (nullable): voxel-frames resolved exactly since the last reset
+/* applies (nullable): whether a bits-only call of max_frames frames on this
+ * handle takes coarse passes; fixups (nullable): voxel-frames resolved exactly since the last reset
  * (synchronous read of a device counter); reset != 0 zeroes the counter. */
 int psfs_coarse_status(psfs_handle *h, int32_t *applies, int64_t *fixups, int32_t reset);
 

@@ -116,6 +116,7 @@ struct S1CParams {
     int32_t rec;         // bytes per code record: 32 (passes) or 1 (debug, nf = 1)
     int32_t ncam, nf;    // frames in this pass (1..32)
     int32_t quarters;    // ceil(nf / 8): 8-frame parts in adjacent blocks
+    int32_t x4;          // 4 pixels per thread (W % 4, ROI columns % 4, frames 4-byte aligned)
     double lr;           // ln(1 - p_O) - ln p_O
     float s;             // 2^(20 - sh)
     float zoff;          // (-ln p_O - eps) s + bias

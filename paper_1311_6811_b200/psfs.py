@@ -115,7 +115,7 @@ def lib():
         L.psfs_peer_status.argtypes = [vp, vp]
         L.psfs_color.argtypes = [vp, vp, vp, vp, C.c_int64, d, vp, vp, vp]
         L.psfs_train_background.argtypes = [vp, i32, i32, vp, vp, vp, i32, vp]
-        L.psfs_set_coarse.argtypes = [vp, i32, i32, C.c_int64]
+        L.psfs_set_coarse.argtypes = [vp, i32, i32, i32, C.c_int64]
         L.psfs_coarse_plan.argtypes = [C.POINTER(Params), i32, vp, C.POINTER(d)]
         L.psfs_coarse_status.argtypes = [vp, C.POINTER(i32), C.POINTER(C.c_int64), i32]
         L.psfs_debug_codes.argtypes = [vp, vp, vp, vp]
@@ -272,12 +272,14 @@ class Reconstructor:
     def set_max_fuse(self, fmax: int):
         self._check(lib().psfs_set_max_fuse(self._h, int(fmax)), "psfs_set_max_fuse")
 
-    def set_coarse(self, mode: int = 1, max_frames: int = MAX_COARSE, fix_capacity: int = 0):
+    def set_coarse(self, mode: int = 1, max_frames: int = MAX_COARSE, min_frames: int = 0,
+                   fix_capacity: int = 0):
         """Coarse passes for bits-only calls: 0 off, 1 on (default), 2 every
-        voxel-frame resolved exactly (test mode); frames per pass 1..32;
-        fix-up list entries (0 = default 2^20)."""
-        self._check(lib().psfs_set_coarse(self._h, int(mode), int(max_frames), int(fix_capacity)),
-                    "psfs_set_coarse")
+        voxel-frame resolved exactly (test mode); frames per pass 1..32; calls
+        with fewer than min_frames frames stay exact (0 = default 16); fix-up
+        list entries (0 = default 2^20)."""
+        self._check(lib().psfs_set_coarse(self._h, int(mode), int(max_frames), int(min_frames),
+                                          int(fix_capacity)), "psfs_set_coarse")
 
     def coarse_status(self, reset: bool = False):
         """(applies to bits-only calls, voxel-frames resolved exactly since the last reset)."""

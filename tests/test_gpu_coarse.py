@@ -35,7 +35,7 @@ def _cuda():
 def _rec(scene, params=None, mode=1, **kw):
     from paper_1311_6811_b200 import from_scene
     rec = from_scene(scene, params or {}, **kw)
-    rec.set_coarse(mode)
+    rec.set_coarse(mode, 32, 1)  # coarse passes for every bits-only call
     return rec
 
 
@@ -101,6 +101,10 @@ def test_c2_bits_identical_to_exact_path(nf, overlap):
     Bb = _bits(b, frames, nf)
     assert torch.equal(Ba, Bb)
     assert int(Ba.ne(0).sum()) > 0
+    if nf < 16:  # the default policy: calls below 16 frames take the exact path
+        a.set_coarse(1)
+        assert torch.equal(_bits(a, frames, nf), Bb)
+        assert a.last_launch_count == 2 * len([g for g in (16, 8, 4, 2, 1) if nf & g])
 
 
 @pytest.mark.parametrize("params", [dict(), dict(occlusion_prior=0.3, voxel_prior=0.2, threshold=0.7),
@@ -115,7 +119,7 @@ def test_fixup_everywhere_equals_exact_path(params, capacity):
     nf = 11
     frames = torch.from_numpy(np.stack([make_frames(s, f) for f in range(nf)])).cuda()
     a = _rec(s, params, mode=2)
-    a.set_coarse(2, 32, capacity)
+    a.set_coarse(2, 32, 1, capacity)
     a.coarse_status(reset=True)
     Ba = _bits(a, frames, nf)
     _, nfix = a.coarse_status(reset=True)
@@ -130,7 +134,7 @@ def test_pass_sizes(max_frames):
     nf = 19
     frames = torch.from_numpy(np.stack([make_frames(s, f) for f in range(nf)])).cuda()
     a = _rec(s)
-    a.set_coarse(1, max_frames)
+    a.set_coarse(1, max_frames, 1)
     b = _rec(s, mode=0)
     assert torch.equal(_bits(a, frames, nf), _bits(b, frames, nf))
 
