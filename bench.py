@@ -464,7 +464,7 @@ def run_ours(args):
     traffic = {}
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(args.config, {})
+            traffic = json.load(f).get(args.config + ("_coarse" if coarse else ""), {})
     except Exception:
         pass
     roi = rec.roi()
@@ -490,7 +490,8 @@ def run_ours(args):
     import torch as _t
     nsm = _t.cuda.get_device_properties(dev).multi_processor_count
     l1_sector_peak = nsm * sm_clk * 1e6 * wf_bytes / 1e9
-    s1_name = "k_likelihood_c8" if coarse else "k_likelihood"
+    s1_name = ("k_likelihood_c8p" if (scene.widths % 4 == 0).all() else "k_likelihood_c8") if coarse \
+        else "k_likelihood"
     s2_name = "k_voxel_c8 + k_fixup_c8" if coarse else ("k_voxel16" if F == 16 else "k_voxel")
     per_kernel = {
         "k_likelihood": {"name": s1_name,

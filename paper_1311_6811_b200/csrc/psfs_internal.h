@@ -117,6 +117,8 @@ struct S1CParams {
     int32_t ncam, nf;    // frames in this pass (1..32)
     int32_t quarters;    // ceil(nf / 8): 8-frame parts in adjacent blocks
     int32_t x4;          // 4 pixels per thread (W % 4, ROI columns % 4, frames 4-byte aligned)
+    int32_t persistent;  // x4: persistent blocks, all quarters per thread (k_likelihood_c8p)
+    int32_t n4;          // x4: 4-pixel groups over all cameras (cam[c].pad_[0] = camera c's first)
     double lr;           // ln(1 - p_O) - ln p_O
     float s;             // 2^(20 - sh)
     float zoff;          // (-ln p_O - eps) s + bias
