@@ -570,8 +570,9 @@ def run_ours(args):
                "d2h_bytes_per_step": int(B * scene.grid.nwords * 4),
                "ms_per_step": e_ms / args.steps,
                "how": "psfs_reconstruct_host: pinned host frames (the region-of-interest rectangle "
-                      "of each image, 2-D copies) -> device staging (copy stream), "
-                      "both stages, bitmask -> pinned host (second copy stream), double-buffered"}
+                      "of each image, read over PCIe by the zero-copy upload kernel k_h2d_rows on a "
+                      "copy stream) -> device staging, both stages, bitmask -> pinned host (second "
+                      "copy stream), double-buffered"}
 
     # ---- secondary: the two kernels in isolation (serial schedule), so their
     # roofline fractions are not diluted by the overlap of the headline schedule

@@ -286,6 +286,16 @@ int psfs_coarse_status(psfs_handle *h, int32_t *applies, int64_t *fixups, int32_
 int psfs_debug_codes(psfs_handle *h, const uint8_t *const *frames, uint8_t *codes_out,
                      void *cuda_stream);
 
+/* How psfs_reconstruct_host moves the frames' region-of-interest rectangles
+ * to the device: mode 1 (default) = when every frame pointer of a group is
+ * page-locked host memory mapped into the device address space (e.g.
+ * cudaHostAlloc / torch pin_memory under unified addressing; checked with
+ * cudaPointerGetAttributes), a copy kernel (k_h2d_rows) reads the rows over
+ * PCIe directly (zero-copy); otherwise, and with mode 0, the DMA engines copy
+ * each rectangle (cudaMemcpy2DAsync).  Results are identical.
+ * Errors: PSFS_EINVAL. */
+int psfs_set_host_upload(psfs_handle *h, int32_t mode);
+
 /* Overlapped batches (default on): with more than one frame group in a
  * psfs_reconstruct_batch call, stage 1 of group g+1 runs on an internal stream
  * beside stage 2 of group g (two term buffers); voxel_blocks_per_sm > 0 caps

@@ -161,6 +161,21 @@ struct VCParams {
 };
 
 cudaError_t launch_likelihood_coarse(const S1CParams &p, int max_roi_px, cudaStream_t s);
+
+// psfs_reconstruct_host upload through mapped pinned memory: warps copy the ROI
+// rows of every (frame, camera) image of a group from host to the staging buffer.
+struct H2DParams {
+    const uint8_t *src[kMaxFC][kMaxCam];  // device-usable addresses of the host images
+    uint8_t *dst;                         // staging: frame f, camera c at dst + f * img_bytes + off[c] * 3
+    int64_t img_bytes;
+    int64_t off[kMaxCam];
+    int32_t W[kMaxCam], r0[kMaxCam], c0[kMaxCam], ncol[kMaxCam];
+    int32_t task_begin[kMaxCam + 1];      // row tasks of camera c in one frame: [task_begin[c], task_begin[c+1])
+    int32_t nf, ncam;
+    int32_t aligned;  // 16: every image and staging image 16-byte aligned with a whole number of
+                      // 16-byte chunks (chunked copy); 4: every row segment 4-byte aligned; 1: bytes
+};
+cudaError_t launch_h2d_rows(const H2DParams &p, int nsm, cudaStream_t s);
 cudaError_t launch_voxel_coarse(const VCParams &p, cudaStream_t s, int *nblocks);
 cudaError_t launch_fixup_coarse(const VCParams &p, cudaStream_t s);
 

@@ -40,7 +40,7 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_set_carve", "psfs_surface", "psfs_smooth_threshold", "psfs_peer_alloc",
            "psfs_peer_open", "psfs_reconstruct_peer", "psfs_peer_status", "psfs_color",
            "psfs_train_background", "psfs_probe_gather_bandwidth", "psfs_set_coarse",
-           "psfs_coarse_plan", "psfs_coarse_status", "psfs_debug_codes"]
+           "psfs_coarse_plan", "psfs_coarse_status", "psfs_debug_codes", "psfs_set_host_upload"]
 MAX_COARSE = 32
 
 
@@ -119,6 +119,7 @@ def lib():
         L.psfs_coarse_plan.argtypes = [C.POINTER(Params), i32, vp, C.POINTER(d)]
         L.psfs_coarse_status.argtypes = [vp, C.POINTER(i32), C.POINTER(C.c_int64), i32]
         L.psfs_debug_codes.argtypes = [vp, vp, vp, vp]
+        L.psfs_set_host_upload.argtypes = [vp, i32]
         _lib = L
     return _lib
 
@@ -287,6 +288,11 @@ class Reconstructor:
         self._check(lib().psfs_coarse_status(self._h, C.byref(a), C.byref(n), int(bool(reset))),
                     "psfs_coarse_status")
         return bool(a.value), int(n.value)
+
+    def set_host_upload(self, mode: int):
+        """psfs_reconstruct_host uploads: 1 zero-copy kernel for mapped pinned frames
+        (default), 0 DMA 2-D copies."""
+        self._check(lib().psfs_set_host_upload(self._h, int(mode)), "psfs_set_host_upload")
 
     def set_carve(self, on: bool):
         """Bits-only early exit (exact bitmask; ignored when log-odds are requested)."""

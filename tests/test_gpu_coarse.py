@@ -182,15 +182,25 @@ def test_ragged_grids(dims, coarse):
     assert torch.equal(_bits(a, frames, nf), _bits(b, frames, nf))
 
 
-def test_host_path_coarse():
+@pytest.mark.parametrize("upload", [1, 0])
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_path_coarse(upload, pinned):
+    """psfs_reconstruct_host, coarse passes: zero-copy upload kernel (mapped pinned
+    frames) or DMA 2-D copies (mode 0, or pageable frames: the kernel path must
+    refuse them), bits identical to the device path."""
     s = make_scene("C2")
     nf = 40
     frames = np.stack([make_frames(s, f % 16) for f in range(nf)])
     a = _rec(s)
-    hf = torch.from_numpy(frames).pin_memory()
+    a.set_host_upload(upload)
+    hf = torch.from_numpy(frames)
+    if pinned:
+        hf = hf.pin_memory()
     Bh = torch.zeros((nf, s.grid.nwords), dtype=torch.int32).pin_memory()
     a.reconstruct_host(hf, nf, None, Bh)
     torch.cuda.synchronize()
+    kernel_used = a.last_launch_count > 3 * 2  # 2 passes x 3 kernels (+ 1 upload kernel each)
+    assert kernel_used == (upload == 1 and pinned)
     b = _rec(s, mode=0)
     assert torch.equal(Bh.cuda(), _bits(b, torch.from_numpy(frames).cuda(), nf))
 
