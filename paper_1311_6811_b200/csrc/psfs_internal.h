@@ -165,8 +165,9 @@ cudaError_t launch_likelihood_coarse(const S1CParams &p, int max_roi_px, cudaStr
 // psfs_reconstruct_host upload through mapped pinned memory: warps copy the ROI
 // rows of every (frame, camera) image of a group from host to the staging buffer.
 struct H2DParams {
-    const uint8_t *src[kMaxFC][kMaxCam];  // device-usable addresses of the host images
-    uint8_t *dst;                         // staging: frame f, camera c at dst + f * img_bytes + off[c] * 3
+    const uint8_t *src[kMaxFC][kMaxCam];  // device-usable addresses of the host images (compacted frames)
+    int32_t fidx[kMaxFC];                 // staging frame slot of compacted frame j
+    uint8_t *dst;                         // staging: frame slot f, camera c at dst + f * img_bytes + off[c] * 3
     int64_t img_bytes;
     int64_t off[kMaxCam];
     int32_t W[kMaxCam], r0[kMaxCam], c0[kMaxCam], ncol[kMaxCam];
