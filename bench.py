@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--fuse", type=int, default=16, help="frames fused per exact-path pass")
     ap.add_argument("--coarse", type=int, default=1, choices=[0, 1],
                     help="coarse passes for the bits-only headline (psfs_set_coarse; 0: exact path)")
-    ap.add_argument("--coarse-frames", type=int, default=32, help="frames per coarse pass")
+    ap.add_argument("--coarse-frames", type=int, default=64, help="frames per coarse pass")
     ap.add_argument("--config", default="C2")
     ap.add_argument("--ty", type=int, default=1)
     ap.add_argument("--kz", type=int, default=4)
@@ -457,8 +457,10 @@ def run_ours(args):
     l1_peak = probe_l1_bandwidth() / 1e9 if not args.profile else None
     # k_voxel16's access pattern measured live: lane pairs on two-sector lines of a
     # 64 MB L2-resident table, non-allocating 256-bit loads (psfs_probe_gather_bandwidth)
-    if coarse:  # k_voxel_c8: one 32-byte sector per lane, 2 blocks/SM, a ~32 MB code table
-        gather_peak = probe_gather_bandwidth(32 << 20, 1, 2) / 1e9 if not args.profile else None
+    wide = coarse and args.coarse_frames > 32  # k_voxel_c8w: 64-byte records, lane pairs
+    if coarse:  # one (narrow) or two (wide) 32-byte sectors per line, 2 blocks/SM, 31 / 62 MB codes
+        gather_peak = (probe_gather_bandwidth((64 if wide else 32) << 20, 2 if wide else 1, 2) / 1e9
+                       if not args.profile else None)
     else:
         gather_peak = probe_gather_bandwidth(64 << 20, 2, 3) / 1e9 if not args.profile else None
     traffic = {}
@@ -484,7 +486,8 @@ def run_ours(args):
     # carrying wf_bytes useful bytes (32: one sector, F = 8; 64: two sectors of
     # one line, F = 16); peak = 1 wavefront/clk/SM x wf_bytes
     v_avg_s = (v_ms / max(v_n, 1)) / 1e3
-    sectors, wf_bytes = gather_sectors(scene, 8 if coarse else F)  # coarse: 32-B records, one per lane
+    # coarse: 32-B records one per lane (narrow), 64-B records by lane pairs (wide, as k_voxel16)
+    sectors, wf_bytes = gather_sectors(scene, 16 if wide else (8 if coarse else F))
     s2_bytes = sectors * wf_bytes
     sm_clk = (clocks or {}).get("sm_mhz") or float(peaks.get("sm_max_mhz", 1965.0))
     import torch as _t
@@ -492,7 +495,8 @@ def run_ours(args):
     l1_sector_peak = nsm * sm_clk * 1e6 * wf_bytes / 1e9
     s1_name = ("k_likelihood_c8p" if (scene.widths % 4 == 0).all() else "k_likelihood_c8") if coarse \
         else "k_likelihood"
-    s2_name = "k_voxel_c8 + k_fixup_c8" if coarse else ("k_voxel16" if F == 16 else "k_voxel")
+    s2_name = (("k_voxel_c8w" if wide else "k_voxel_c8") + " + k_fixup_c8") if coarse else \
+        ("k_voxel16" if F == 16 else "k_voxel")
     per_kernel = {
         "k_likelihood": {"name": s1_name,
             "bound": "hbm", "achieved": s1_bytes / s1_avg_s / 1e9, "peak": hbm_peak,
@@ -515,11 +519,15 @@ def run_ours(args):
                                        "peak_source": kv["peak_source"]}
         kv.update({"bound": "l2_gather", "peak": gather_peak,
                    "fixups_per_step": fixups / max(args.steps, 1),
-                   "peak_source": "measured live: psfs_probe_gather_bandwidth(32 MB, 1 sector/line, "
-                                  "2 blocks/SM) -- every lane reads one 32-byte sector of its own "
-                                  "random 128-byte line of an L2-resident table with k_voxel_c8's "
-                                  "non-allocating 256-bit load and residency; the timed launch "
-                                  "includes k_fixup_c8; DESIGN.md section 8"})
+                   "peak_source": ("measured live: psfs_probe_gather_bandwidth(64 MB, 2 sectors/line, "
+                                   "2 blocks/SM) -- lane pairs read both 32-byte sectors of random "
+                                   "128-byte lines of an L2-resident table (k_voxel_c8w's pattern)"
+                                   if wide else
+                                   "measured live: psfs_probe_gather_bandwidth(32 MB, 1 sector/line, "
+                                   "2 blocks/SM) -- every lane reads one 32-byte sector of its own "
+                                   "random 128-byte line of an L2-resident table (k_voxel_c8's pattern)")
+                                  + ", non-allocating 256-bit loads at the kernel's residency; the "
+                                    "timed launch includes k_fixup_c8; DESIGN.md section 8"})
     elif F == 16 and gather_peak:
         # the binding roofline of the 16-frame gather: the same access pattern's
         # measured rate from L2 (the all-hit L1 line rate kept beside it)

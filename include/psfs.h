@@ -170,8 +170,11 @@ int psfs_reconstruct_batch(psfs_handle *h, int32_t nframes, const uint8_t *const
  * device staging buffers on
  * an internal copy stream, computes on cuda_stream, and copies the results back
  * on a second copy stream, double-buffered so group g+1's upload and group
- * g-1's download overlap group g's kernels.  Asynchronous: host outputs are
- * valid once cuda_stream has reached the end of the call (synchronize it).
+ * g-1's download overlap group g's kernels (and a call's upload the previous
+ * call's kernels).  Asynchronous: the host frames are read from the time of the
+ * call on (they must not be the destination of copies still pending on
+ * cuda_stream); host outputs are valid once cuda_stream has reached the end of
+ * the call (synchronize it).
  * Same errors as psfs_reconstruct_batch, plus PSFS_ENOMEM for the staging. */
 int psfs_reconstruct_host(psfs_handle *h, int32_t nframes, const uint8_t *const *frames,
                           float *logodds, uint32_t *bits, void *cuda_stream);
@@ -247,7 +250,8 @@ int psfs_set_carve(psfs_handle *h, int32_t enabled);
  * P:111 / R#14 needs only the sign of L - logit tau).  When a reconstruct call
  * requests no log-odds, stage 1 stores an 8-bit code per pixel and frame that
  * brackets the exact Q11.20 term q of Eq 5-9 (c 2^sh <= q <= c 2^sh + wc), 32
- * frames per 32-byte record; stage 2 sums the codes of every voxel's cameras
+ * frames per 32-byte record (33..64 frames: 64-byte records read by lane
+ * pairs); stage 2 sums the codes of every voxel's cameras
  * and decides every voxel-frame whose bracket lies on one side of T_q; the
  * others (rare: |L - logit tau| within about ncam * 2^(sh-20)) are summed
  * exactly from the frames and the model with the exact path's per-pixel
@@ -258,7 +262,7 @@ int psfs_set_carve(psfs_handle *h, int32_t enabled);
  * the voxel kernel (slow, still exact).
  * mode: 0 = off (always the exact int32 path), 1 = on (default), 2 = test mode
  * (every voxel-frame resolved exactly through the fix-up).  max_frames: frames
- * per coarse pass, 1..32 (default 32; a call's frames are split into balanced
+ * per coarse pass, 1..64 (default 64, at most 2048 / ncam; a call's frames are split into balanced
  * passes).  min_frames: calls with fewer frames take the exact path, which is
  * faster for small batches (0 = default 16).  fix_capacity: list entries (8
  * bytes each), 0 = default 2^20.  Coarse passes apply when the params

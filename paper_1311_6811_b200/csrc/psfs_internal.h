@@ -106,14 +106,15 @@ struct VParams {
 // its error bound); the 32 frames of a pass share one 32-byte record.  Stage 2
 // sums codes, decides every voxel-frame whose bounds lie on one side of T_q, and
 // recomputes the rest exactly (the same per-pixel arithmetic as k_likelihood).
-constexpr int kMaxFC = 32;  // frames per coarse pass (one byte each per record)
+constexpr int kMaxFC = 64;       // frames per coarse pass (one byte each per record)
+constexpr int kMaxFramePtrs = 2048;  // frames x cameras of one coarse pass (kernel-parameter table)
 
 struct S1CParams {
     S1Cam cam[kMaxCam];                      // ROI, model / code offsets (tstride = row stride)
-    const uint8_t *frames[kMaxFC][kMaxCam];  // [f][c], f < nf
+    const uint8_t *frames[kMaxFramePtrs];  // [f * ncam + c], f < nf
     const struct ModelPx *model;
     uint8_t *codes;      // (toff + p) * rec + f
-    int32_t rec;         // bytes per code record: 32 (passes) or 1 (debug, nf = 1)
+    int32_t rec;         // bytes per code record: 32 (passes of <= 32 frames), 64 (<= 64), 1 (debug, nf = 1)
     int32_t ncam, nf;    // frames in this pass (1..32)
     int32_t quarters;    // ceil(nf / 8): 8-frame parts in adjacent blocks
     int32_t x4;          // 4 pixels per thread (W % 4, ROI columns % 4, frames 4-byte aligned)
@@ -134,9 +135,10 @@ struct VCCam {
 
 struct VCParams {
     VCCam cam[kMaxCam];
-    const uint8_t *frames[kMaxFC][kMaxCam];  // fix-up: the exact terms are recomputed
+    const uint8_t *frames[kMaxFramePtrs];  // [f * ncam + c]; fix-up: the exact terms are recomputed
     const struct ModelPx *model;
-    const uint8_t *codes;     // 32-byte records
+    const uint8_t *codes;     // 32- or 64-byte records (rec)
+    int32_t rec;
     uint32_t K0, K1;          // packed 16-bit thresholds: field >= K1 -> bit 1; K0 <= field < K1 -> exact
     int32_t Tq;
     int32_t ncam, nf;
@@ -152,7 +154,7 @@ struct VCParams {
     uint32_t *peer[kMaxPeers];
     int64_t peer_fstride;
     unsigned long long *fix_count;  // nullable: voxel-frames resolved exactly
-    // undecided voxel-frames: (v << 5 | frame) appended at fix_list[*fix_head], then
+    // undecided voxel-frames: (v << 6 | frame) appended at fix_list[*fix_head], then
     // k_fixup_c8 sums them exactly and patches the bits; beyond fix_cap the lane
     // resolves them in place (slow, correct)
     unsigned long long *fix_list;
@@ -165,7 +167,7 @@ cudaError_t launch_likelihood_coarse(const S1CParams &p, int max_roi_px, cudaStr
 // psfs_reconstruct_host upload through mapped pinned memory: warps copy the ROI
 // rows of every (frame, camera) image of a group from host to the staging buffer.
 struct H2DParams {
-    const uint8_t *src[kMaxFC][kMaxCam];  // device-usable addresses of the host images (compacted frames)
+    const uint8_t *src[kMaxFramePtrs];    // [j * ncam + c]: device-usable addresses of the host images
     int32_t fidx[kMaxFC];                 // staging frame slot of compacted frame j
     uint8_t *dst;                         // staging: frame slot f, camera c at dst + f * img_bytes + off[c] * 3
     int64_t img_bytes;

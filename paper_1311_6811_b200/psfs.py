@@ -41,7 +41,7 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_peer_open", "psfs_reconstruct_peer", "psfs_peer_status", "psfs_color",
            "psfs_train_background", "psfs_probe_gather_bandwidth", "psfs_set_coarse",
            "psfs_coarse_plan", "psfs_coarse_status", "psfs_debug_codes", "psfs_set_host_upload"]
-MAX_COARSE = 32
+MAX_COARSE = 64
 
 
 class PsfsError(RuntimeError):
@@ -276,7 +276,7 @@ class Reconstructor:
     def set_coarse(self, mode: int = 1, max_frames: int = MAX_COARSE, min_frames: int = 0,
                    fix_capacity: int = 0):
         """Coarse passes for bits-only calls: 0 off, 1 on (default), 2 every
-        voxel-frame resolved exactly (test mode); frames per pass 1..32; calls
+        voxel-frame resolved exactly (test mode); frames per pass 1..64; calls
         with fewer than min_frames frames stay exact (0 = default 16); fix-up
         list entries (0 = default 2^20)."""
         self._check(lib().psfs_set_coarse(self._h, int(mode), int(max_frames), int(min_frames),

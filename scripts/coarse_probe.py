@@ -12,7 +12,7 @@ from synth.scene import make_frames, make_scene  # noqa: E402
 
 
 def main():
-    nf = int(sys.argv[1]) if len(sys.argv) > 1 else 32
+    nf = int(sys.argv[1]) if len(sys.argv) > 1 else 64
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
     s = make_scene("C2")
     frames = torch.from_numpy(np.stack([make_frames(s, f % 16) for f in range(nf)])).cuda()

@@ -35,7 +35,7 @@ def _cuda():
 def _rec(scene, params=None, mode=1, **kw):
     from paper_1311_6811_b200 import from_scene
     rec = from_scene(scene, params or {}, **kw)
-    rec.set_coarse(mode, 32, 1)  # coarse passes for every bits-only call
+    rec.set_coarse(mode, 64, 1)  # coarse passes for every bits-only call
     return rec
 
 
@@ -96,7 +96,7 @@ def test_c2_bits_identical_to_exact_path(nf, overlap):
     a.set_overlap(overlap, 0)
     assert a.coarse_status()[0]
     Ba = _bits(a, frames, nf)
-    assert a.last_launch_count == 3 * ((nf + 31) // 32)  # k_likelihood_c8, k_voxel_c8, k_fixup_c8
+    assert a.last_launch_count == 3 * ((nf + 63) // 64)  # k_likelihood_c8p, k_voxel_c8(w), k_fixup_c8
     b = _rec(s, mode=0)
     Bb = _bits(b, frames, nf)
     assert torch.equal(Ba, Bb)
@@ -110,16 +110,16 @@ def test_c2_bits_identical_to_exact_path(nf, overlap):
 @pytest.mark.parametrize("params", [dict(), dict(occlusion_prior=0.3, voxel_prior=0.2, threshold=0.7),
                                     dict(occlusion_prior=0.05, threshold=0.3)])
 @pytest.mark.parametrize("capacity", [0, 1000])
-def test_fixup_everywhere_equals_exact_path(params, capacity):
+@pytest.mark.parametrize("nf", [11, 40])
+def test_fixup_everywhere_equals_exact_path(params, capacity, nf):
     """Test mode 2 sends every voxel-frame through the exact fix-up: listed and
     summed by k_fixup_c8 (capacity 2^20), or, past a 1000-entry list, summed in
     place by k_voxel_c8 (coarse_exact_sum).  The result must still be the exact
     path's bitmask."""
     s = make_scene("C1")
-    nf = 11
-    frames = torch.from_numpy(np.stack([make_frames(s, f) for f in range(nf)])).cuda()
+    frames = torch.from_numpy(np.stack([make_frames(s, f % 13) for f in range(nf)])).cuda()
     a = _rec(s, params, mode=2)
-    a.set_coarse(2, 32, 1, capacity)
+    a.set_coarse(2, 64, 1, capacity)
     a.coarse_status(reset=True)
     Ba = _bits(a, frames, nf)
     _, nfix = a.coarse_status(reset=True)
@@ -128,10 +128,12 @@ def test_fixup_everywhere_equals_exact_path(params, capacity):
     assert torch.equal(Ba, _bits(b, frames, nf))
 
 
-@pytest.mark.parametrize("max_frames", [1, 7, 8, 9, 32])
+@pytest.mark.parametrize("max_frames", [1, 7, 8, 9, 32, 33, 40, 64])
 def test_pass_sizes(max_frames):
+    """Narrow (<= 32 frames, k_voxel_c8) and wide (33..64, k_voxel_c8w) passes,
+    partial quarters, balanced splits of 70 frames."""
     s = make_scene("C1")
-    nf = 19
+    nf = 70
     frames = torch.from_numpy(np.stack([make_frames(s, f) for f in range(nf)])).cuda()
     a = _rec(s)
     a.set_coarse(1, max_frames, 1)
@@ -189,7 +191,7 @@ def test_host_path_coarse(upload, pinned):
     frames) or DMA 2-D copies (mode 0, or pageable frames: the kernel path must
     refuse them), bits identical to the device path."""
     s = make_scene("C2")
-    nf = 40
+    nf = 80
     frames = np.stack([make_frames(s, f % 16) for f in range(nf)])
     a = _rec(s)
     a.set_host_upload(upload)
@@ -199,7 +201,9 @@ def test_host_path_coarse(upload, pinned):
     Bh = torch.zeros((nf, s.grid.nwords), dtype=torch.int32).pin_memory()
     a.reconstruct_host(hf, nf, None, Bh)
     torch.cuda.synchronize()
-    kernel_used = a.last_launch_count > 3 * 2  # 2 passes x 3 kernels (+ 1 upload kernel each)
+    passes = (nf + 63) // 64  # 3 kernels per pass (+ 1 upload kernel each on the zero-copy path)
+    assert a.last_launch_count in (3 * passes, 4 * passes)
+    kernel_used = a.last_launch_count == 4 * passes
     assert kernel_used == (upload == 1 and pinned)
     b = _rec(s, mode=0)
     assert torch.equal(Bh.cuda(), _bits(b, torch.from_numpy(frames).cuda(), nf))
