@@ -265,7 +265,8 @@ int psfs_set_carve(psfs_handle *h, int32_t enabled);
  * per coarse pass, 1..64 (default 64, at most 2048 / ncam; a call's frames are split into balanced
  * passes).  min_frames: calls with fewer frames take the exact path, which is
  * faster for small batches (0 = default 16).  fix_capacity: list entries (8
- * bytes each), 0 = default 2^20.  Coarse passes apply when the params
+ * bytes each), 0 = automatic (1/1024 of a 64-frame pass's voxel-frames, within
+ * 2^20 .. 2^26).  Coarse passes apply when the params
  * admit them (psfs_coarse_plan), xlen % 32 == 0, the tile depth kz <= 8 and
  * carve is off; otherwise calls take the exact path. */
 int psfs_set_coarse(psfs_handle *h, int32_t mode, int32_t max_frames, int32_t min_frames,
