@@ -227,3 +227,39 @@ def test_coarse_bits_vs_oracle(name, params):
                                        tau=params.get("threshold", 0.5))
         st = assert_parity(None, B[f], orc, s.grid.nvox, tau=params.get("threshold", 0.5))
         assert st["occupied"] > 0
+
+
+@pytest.mark.parametrize("name,nf", [("C4", 40)])
+def test_full_size_wide_pass_vs_oracle(name, nf):
+    """C4 (512^3, 16 cameras at 1920x1080) in one wide coarse pass (k_voxel_c8w with
+    NCAM = 16): 2 distinct frame sets repeated; both checked against the oracle on a
+    voxel sample (every 64th slice x 4096 voxels + 65536 random voxels), every
+    repeat bit-identical to its original, and the whole bitmask equal to the exact
+    int32 path's."""
+    s = make_scene(name)
+    two = [make_frames(s, 0), make_frames(s, 1)]
+    fr = torch.from_numpy(np.stack(two)).cuda().repeat(nf // 2, 1, 1, 1, 1)
+    a = _rec(s)
+    a.coarse_status(reset=True)
+    Ba = _bits(a, fr, nf)
+    assert a.last_launch_count == 3
+    _, nfix = a.coarse_status(reset=True)
+    for f in range(2, nf):
+        assert torch.equal(Ba[f], Ba[f % 2])
+    rng = np.random.default_rng(13)
+    plane = s.grid.xlen * s.grid.ylen
+    vox = np.unique(np.concatenate([np.concatenate([k * plane + rng.integers(0, plane, 4096)
+                                                    for k in range(0, s.grid.zlen, 64)]),
+                                    rng.integers(0, s.grid.nvox, 1 << 16)]))
+    vt = torch.from_numpy(vox).cuda()
+    for f in range(2):
+        _, post = oracle.fuse_sample(s.P, s.widths, s.heights, s.grid, two[f], s.mu, s.sigma, vox,
+                                     nthreads=NTHREADS)
+        words = Ba[f][(vt >> 5)].cpu().numpy().view(np.uint32)
+        bits = ((words >> (vox & 31).astype(np.uint32)) & 1).astype(bool)
+        assert not ((bits != (post > 0.5)) & ~(np.abs(post - 0.5) < 1e-4)).any()
+        assert bits.sum() > 0
+    b = _rec(s, mode=0)
+    Bb = _bits(b, fr[:2].contiguous(), 2)
+    assert torch.equal(Ba[:2], Bb)
+    assert 0 < nfix < 1e-3 * nf * s.grid.nvox
