@@ -272,11 +272,13 @@ int psfs_set_carve(psfs_handle *h, int32_t enabled);
 int psfs_set_coarse(psfs_handle *h, int32_t mode, int32_t max_frames, int32_t min_frames,
                     int64_t fix_capacity);
 
-/* Host-only: the coarse-code plan for params and ncam cameras.  out (HOST, 4
+/* Host-only: the coarse-code plan for params and ncam cameras.  out (HOST, 7
  * int32): admitted (sigma_floor >= 0.25 and p_O in [1e-3, 1 - 1e-3]), sh (code
  * quantum 2^sh in Q11.20 units), bias (the code of t = 0), wc (bracket width:
- * q in [c 2^sh, c 2^sh + wc]); eps (nullable): the FP32 error bound in t the
- * bracket is widened by. */
+ * q in [c 2^sh, c 2^sh + wc]), K0, K1 (a voxel-frame whose code sum U = sum
+ * over the cameras of (c + bias) has U >= K1 is occupied, U < K0 unoccupied,
+ * otherwise summed exactly), T_q (occupied <=> S > T_q); eps (nullable): the
+ * FP32 error bound in t the bracket is widened by. */
 int psfs_coarse_plan(const psfs_params *params, int32_t ncam, int32_t *out, double *eps);
 
 /* applies (nullable): whether a bits-only call of max_frames frames on this

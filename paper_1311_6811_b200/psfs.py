@@ -137,12 +137,13 @@ def coarse_plan(params: dict | None = None, ncam: int = 8) -> dict:
     lib().psfs_default_params(C.byref(p))
     for k, v in (params or {}).items():
         setattr(p, k, float(v))
-    out = np.zeros(4, np.int32)
+    out = np.zeros(7, np.int32)
     eps = C.c_double()
     rc = lib().psfs_coarse_plan(C.byref(p), int(ncam), out.ctypes.data, C.byref(eps))
     if rc != PSFS_OK:
         raise PsfsError(rc, "psfs_coarse_plan")
-    return dict(ok=bool(out[0]), sh=int(out[1]), bias=int(out[2]), wc=int(out[3]), eps=eps.value)
+    return dict(ok=bool(out[0]), sh=int(out[1]), bias=int(out[2]), wc=int(out[3]), K0=int(out[4]),
+                K1=int(out[5]), Tq=int(out[6]), eps=eps.value)
 
 
 def _ptr_array(ptrs):

@@ -53,3 +53,32 @@ def test_plan_default_is_sixteen():
 def test_plan_rejects_unbounded_params(params):
     """Outside the admitted range the FP32 error bound is not claimed: exact path."""
     assert not psfs.coarse_plan(params, 8)["ok"]
+
+
+@pytest.mark.parametrize("params", [dict(), dict(occlusion_prior=0.3, voxel_prior=0.2, threshold=0.7),
+                                    dict(occlusion_prior=0.05, threshold=0.3), dict(sigma_floor=0.5),
+                                    dict(voxel_prior=0.9, threshold=0.2)])
+@pytest.mark.parametrize("ncam", [1, 4, 8, 16, 32])
+def test_thresholds_decide_exactly_where_the_bracket_allows(params, ncam):
+    """Brute force over every code sum U = sum(c + bias) of ncam cameras: the exact
+    S lies in [2^sh sum c, 2^sh sum c + ncam wc] (each camera's bracket; an
+    out-of-view camera's exact 0 is in its c = 0 bracket).  U >= K1 must imply S >
+    T_q for every S in that range, U < K0 must imply S <= T_q, and every U in
+    [K0, K1) must leave both outcomes possible (nothing decided that needs no fix-up
+    is sent to it, nothing undecided is decided)."""
+    p = psfs.coarse_plan(params, ncam)
+    assert p["ok"]
+    q, wc, bias, Tq, K0, K1 = 1 << p["sh"], p["wc"], p["bias"], p["Tq"], p["K0"], p["K1"]
+    # T_q from the definition: floor((logit tau - logit p_V) 2^20) (DESIGN.md section 6)
+    tau, pv = params.get("threshold", 0.5), params.get("voxel_prior", 0.5)
+    assert Tq == math.floor((math.log(tau / (1 - tau)) - math.log(pv / (1 - pv))) * 2 ** 20)
+    assert 0 <= K0 <= K1 <= 32767
+    for U in range(0, 255 * ncam + 1):
+        sc = U - ncam * bias
+        lo, hi = q * sc, q * sc + ncam * wc
+        if U >= K1:
+            assert lo > Tq, (U, lo, Tq)
+        elif U < K0:
+            assert hi <= Tq, (U, hi, Tq)
+        else:
+            assert lo <= Tq < hi, (U, lo, hi, Tq)
