@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-zslab", action="store_true", help="skip the C4 z-slab section")
+    ap.add_argument("--zslab-frames", type=int, default=64, help="frame sets per z-slab call (even)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true",
@@ -671,11 +672,11 @@ def run_ours(args):
             from synth.scene import make_frames, make_scene
             zs = make_scene("C4")
             two = torch.from_numpy(np.stack([make_frames(zs, f) for f in range(2)])).to(dev)
-            zfr = two.repeat(8, 1, 1, 1, 1)  # 16 frame sets (2 distinct, host rendering is slow)
+            zfr = two.repeat(args.zslab_frames // 2, 1, 1, 1, 1)  # 2 distinct (host rendering is slow)
             del two
             zslab = zslab_bench(args, zs, zfr, rank, world, local, dev, stream)
             zslab["config"] = ("C4: 512^3 grid, 16 cameras at 1920x1080, z-slab partition over "
-                               f"{world} GPU(s), 16 frame sets per call (2 distinct, repeated)")
+                               f"{world} GPU(s), {args.zslab_frames} frame sets per call (2 distinct, repeated)")
             del zfr
         except Exception as e:  # reported, never fatal for the headline
             zslab = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
