@@ -260,6 +260,9 @@ int psfs_set_carve(psfs_handle *h, int32_t enabled);
  * second kernel (k_fixup_c8, one warp per entry, cameras across the lanes) that
  * patches their bits; entries beyond the list's capacity are summed in place by
  * the voxel kernel (slow, still exact).
+ * psfs_reconstruct_peer uses coarse passes only when this device has native
+ * atomics to every other visible device (NVLink / NVSwitch; checked by
+ * psfs_peer_open), since the fix-up patches bits in every rank's buffer.
  * mode: 0 = off (always the exact int32 path), 1 = on (default), 2 = test mode
  * (every voxel-frame resolved exactly through the fix-up).  max_frames: frames
  * per coarse pass, 1..64 (default 64, at most 2048 / ncam; a call's frames are split into balanced
