@@ -261,8 +261,8 @@ int psfs_set_carve(psfs_handle *h, int32_t enabled);
  * patches their bits; entries beyond the list's capacity are summed in place by
  * the voxel kernel (slow, still exact).
  * psfs_reconstruct_peer uses coarse passes only when this device has native
- * atomics to every other visible device (NVLink / NVSwitch; checked by
- * psfs_peer_open), since the fix-up patches bits in every rank's buffer.
+ * atomics to every device that holds a peer buffer (NVLink / NVSwitch; checked
+ * by psfs_peer_open), since the fix-up patches bits in every rank's buffer.
  * mode: 0 = off (always the exact int32 path), 1 = on (default), 2 = test mode
  * (every voxel-frame resolved exactly through the fix-up).  max_frames: frames
  * per coarse pass, 1..64 (default 64, at most 2048 / ncam; a call's frames are split into balanced
@@ -364,7 +364,10 @@ int psfs_color(psfs_handle *h, const uint8_t *const *frames, const int64_t *indi
  *   overwrites a buffer still being read), both stages with peer stores, exit
  *   barrier.  Every rank must make the same sequence of calls.  Asynchronous
  *   on cuda_stream.  A barrier that waits more than ~10 s for a peer gives up
- *   and records the failure, which psfs_peer_status reports.
+ *   and records the failure, which psfs_peer_status reports.  Ragged rows
+ *   (xlen % 8 != 0) OR bits into the peers' words atomically: without native
+ *   peer atomics to every buffer's device (psfs_peer_open) the call returns
+ *   PSFS_ESTATE before any work (use the caller's all-gather instead).
  * psfs_peer_status: synchronizes cuda_stream; PSFS_ETIMEOUT if a barrier timed
  *   out since the last call, else PSFS_OK. */
 int psfs_peer_alloc(psfs_handle *h, int32_t nframes, uint32_t **bits_out, void *ipc_handle_out);

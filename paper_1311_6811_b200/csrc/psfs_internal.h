@@ -164,6 +164,22 @@ struct VCParams {
 
 cudaError_t launch_likelihood_coarse(const S1CParams &p, int max_roi_px, cudaStream_t s);
 
+// Pad records of the padded term / code images.  A buffer's record size changes
+// with the pass (terms: 4F bytes, F = 1..16; codes: 32 or 64 bytes), and the pad
+// records of one size overlap pixel records of another, so the host runtime
+// rewrites them (k_fill_pads) whenever a buffer is about to be used with a
+// record size other than its last one.
+struct PadParams {
+    uint32_t *buf;
+    uint32_t toff[kMaxCam];          // first padded pixel of camera c
+    int32_t W[kMaxCam], H[kMaxCam];
+    int32_t first[kMaxCam + 1];      // pad pixels of camera c: [first[c], first[c+1]), W + H + 1 each
+    int32_t ncam;
+    int32_t rec_words;               // 32-bit words per record
+    uint32_t fill;                   // 0 (terms) or bias * 0x01010101 (codes)
+};
+cudaError_t launch_fill_pads(const PadParams &p, cudaStream_t s);
+
 // psfs_reconstruct_host upload through mapped pinned memory: warps copy the ROI
 // rows of every (frame, camera) image of a group from host to the staging buffer.
 struct H2DParams {
