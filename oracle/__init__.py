@@ -72,6 +72,15 @@ def lib():
         _lib.oracle_color.argtypes = [C.POINTER(_Rig), C.POINTER(_Grid), vp, vp, vp, d, d, i64,
                                       vp, vp, vp, vp]
         _lib.oracle_train_background.argtypes = [i, i64, vp, d, vp, vp]
+        _lib.oracle_train_background_elems.argtypes = [i, i64, vp, d, vp, vp]
+        _lib.oracle_pixel_nch.argtypes = [i, vp, vp, vp, d, d, vp, vp, vp]
+        _lib.oracle_slm_image_nch.argtypes = [i, i64, vp, vp, vp, d, d, vp, vp, vp, i]
+        _lib.oracle_project_pinned_uv.argtypes = [vp, i, i, i, i, i, vp, vp]
+        _lib.oracle_project_pinned_uv.restype = i
+        _lib.oracle_bilinear.argtypes = [vp, i, i, d, d]
+        _lib.oracle_bilinear.restype = d
+        _lib.oracle_fuse_bilinear.argtypes = [C.POINTER(_Rig), C.POINTER(_Grid), vp, d, d, i, i,
+                                              vp, vp, vp, i]
     return _lib
 
 
@@ -95,20 +104,38 @@ def view_likelihood(slm: float, p_occ: float = 0.5):
 def slm_image(img, mu, sigma, sigma_floor=1.0, p_occ=0.5, nthreads=1):
     """Per-pixel SLM (Eq 1-2) and per-view log-likelihoods (Eq 5-9).
 
-    img uint8 [..., 3]; mu, sigma float32 [..., 3] (same leading shape).
+    img uint8 [..., nch]; mu, sigma float32 [..., nch] (same leading shape);
+    nch = 3 (RGB, oracle_slm_image) or any other channel count, e.g. 1 for
+    grayscale (oracle_slm_image_nch, U = 256^-nch; NEXT-3, R#25).
     Returns (slm, lnp1, lnp0) float64 arrays of the leading shape."""
     img = np.ascontiguousarray(img, dtype=np.uint8)
     mu = np.ascontiguousarray(mu, dtype=np.float32)
     sigma = np.ascontiguousarray(sigma, dtype=np.float32)
     shape = img.shape[:-1]
+    nch = img.shape[-1]
     n = int(np.prod(shape)) if shape else 1
-    assert img.shape[-1] == 3 and mu.shape == img.shape and sigma.shape == img.shape
+    assert mu.shape == img.shape and sigma.shape == img.shape
     slm = np.empty(n, np.float64)
     l1 = np.empty(n, np.float64)
     l0 = np.empty(n, np.float64)
-    lib().oracle_slm_image(n, 1, _p(img), _p(mu), _p(sigma), float(sigma_floor), float(p_occ),
-                           _p(slm), _p(l1), _p(l0), int(nthreads))
+    if nch == 3:
+        lib().oracle_slm_image(n, 1, _p(img), _p(mu), _p(sigma), float(sigma_floor), float(p_occ),
+                               _p(slm), _p(l1), _p(l0), int(nthreads))
+    else:
+        lib().oracle_slm_image_nch(int(nch), n, _p(img), _p(mu), _p(sigma), float(sigma_floor),
+                                   float(p_occ), _p(slm), _p(l1), _p(l0), int(nthreads))
     return slm.reshape(shape), l1.reshape(shape), l0.reshape(shape)
+
+
+def pixel_nch(I, mu, sigma, sigma_floor=1.0, p_occ=0.5):
+    """One pixel of any channel count (oracle_pixel_nch): (slm, lnp1, lnp0)."""
+    I = np.ascontiguousarray(np.asarray(I, np.uint8).reshape(-1))
+    mu = np.ascontiguousarray(np.asarray(mu, np.float32).reshape(-1))
+    sigma = np.ascontiguousarray(np.asarray(sigma, np.float32).reshape(-1))
+    a, b, c = C.c_double(), C.c_double(), C.c_double()
+    lib().oracle_pixel_nch(int(I.size), _p(I), _p(mu), _p(sigma), float(sigma_floor), float(p_occ),
+                           C.byref(a), C.byref(b), C.byref(c))
+    return a.value, b.value, c.value
 
 
 # ---------------------------------------------------------------- projection
@@ -130,6 +157,24 @@ def project_pinned(A, W, H, ijk) -> np.ndarray:
     out = np.empty_like(ijk)
     lib().oracle_project_pinned_batch(_p(A), int(W), int(H), ijk.shape[0], _p(ijk), _p(out))
     return out
+
+
+def project_pinned_uv(A, W, H, i, j, k):
+    """The pinned projection's float (u, v) (the +1/2 folded in) and the in-view
+    decision; (0, nan, nan) when out of view (NEXT-3 bilinear, R#26)."""
+    A = np.ascontiguousarray(np.asarray(A, np.float32).reshape(12))
+    u, v = C.c_float(np.nan), C.c_float(np.nan)
+    r = lib().oracle_project_pinned_uv(_p(A), int(W), int(H), int(i), int(j), int(k),
+                                       C.byref(u), C.byref(v))
+    return r, u.value, v.value
+
+
+def bilinear(img, x, y):
+    """oracle_bilinear: bilinear sample of a 2-D float64 image at the continuous
+    pixel position (x, y), neighbours clamped to the image."""
+    img = np.ascontiguousarray(np.asarray(img, np.float64))
+    H, W = img.shape
+    return float(lib().oracle_bilinear(_p(img), int(W), int(H), float(x), float(y)))
 
 
 def project_exact(P, origin, spacing, W, H, i, j, k):
@@ -162,10 +207,13 @@ def _ptrs(arrs):
 
 
 def reconstruct(P, W, H, grid, frames, mu, sigma, sigma_floor=1.0, p_occ=0.5, p_vox=0.5,
-                tau=0.5, k0=0, k1=None, nthreads=1, want_slm=False):
+                tau=0.5, k0=0, k1=None, nthreads=1, want_slm=False, sampling="nearest"):
     """Whole-grid oracle: Eq (1)-(9) per pixel, Eq (3)-(4) per voxel, threshold.
 
-    frames / mu / sigma: per camera [H, W, 3] (uint8 / float32 / float32).
+    frames / mu / sigma: per camera [H, W, nch] (uint8 / float32 / float32),
+    nch = 3 (RGB) or 1 (grayscale, NEXT-3).  sampling: "nearest" (R#10, the
+    hot path) or "bilinear" (NEXT-3, R#26: oracle_fuse_bilinear on the
+    SLM images).
     Returns dict(L=float64 [nvox_slab], post=float64, bits=uint32 words of the
     slab [k0,k1), lnp1/lnp0 per camera, A=the pre-composed matrices)."""
     k1 = grid.zlen if k1 is None else k1
@@ -183,9 +231,17 @@ def reconstruct(P, W, H, grid, frames, mu, sigma, sigma_floor=1.0, p_occ=0.5, p_
     L = np.empty(n, np.float64)
     post = np.empty(n, np.float64)
     bits = np.zeros((n + 31) // 32, np.uint32)
-    p1, p0 = _ptrs(l1s), _ptrs(l0s)
-    lib().oracle_fuse(C.byref(rh.rig), C.byref(g), _p(p1), _p(p0), float(p_vox), float(tau),
-                      int(k0), int(k1), _p(L), _p(post), _p(bits), int(nthreads))
+    if sampling == "bilinear":
+        sl = [np.ascontiguousarray(x.reshape(-1), np.float64) for x in slms]
+        lib().oracle_fuse_bilinear(C.byref(rh.rig), C.byref(g), _p(_ptrs(sl)), float(p_vox),
+                                   float(tau), int(k0), int(k1), _p(L), _p(post), _p(bits),
+                                   int(nthreads))
+    elif sampling == "nearest":
+        p1, p0 = _ptrs(l1s), _ptrs(l0s)
+        lib().oracle_fuse(C.byref(rh.rig), C.byref(g), _p(p1), _p(p0), float(p_vox), float(tau),
+                          int(k0), int(k1), _p(L), _p(post), _p(bits), int(nthreads))
+    else:
+        raise ValueError(sampling)
     out = dict(L=L, post=post, bits=bits, lnp1=l1s, lnp0=l0s, A=A)
     if want_slm:
         out["slm"] = slms
@@ -208,6 +264,25 @@ def fuse_views(P, W, H, grid, lnp1, lnp0, p_occ=0.5, p_vox=0.5, tau=0.5, k0=0, k
     bits = np.zeros((n + 31) // 32, np.uint32)
     lib().oracle_fuse(C.byref(rh.rig), C.byref(g), _p(_ptrs(l1s)), _p(_ptrs(l0s)), float(p_vox),
                       float(tau), int(k0), int(k1), _p(L), _p(post), _p(bits), int(nthreads))
+    return dict(L=L, post=post, bits=bits)
+
+
+def fuse_bilinear_slm(P, W, H, grid, slm, p_occ=0.5, p_vox=0.5, tau=0.5, k0=0, k1=None,
+                      nthreads=1):
+    """NEXT-3 bilinear fusion (oracle_fuse_bilinear) from given per-camera SLM
+    images (float64 [H, W], e.g. hand-set for the pins)."""
+    k1 = grid.zlen if k1 is None else k1
+    A = precompose(P, grid.origin, grid.spacing)
+    rh = _RigHolder(A, W, H, p_occ)
+    g = _grid(grid)
+    sl = [np.ascontiguousarray(np.asarray(a, np.float64).reshape(-1)) for a in slm]
+    n = grid.xlen * grid.ylen * (k1 - k0)
+    L = np.empty(n, np.float64)
+    post = np.empty(n, np.float64)
+    bits = np.zeros((n + 31) // 32, np.uint32)
+    lib().oracle_fuse_bilinear(C.byref(rh.rig), C.byref(g), _p(_ptrs(sl)), float(p_vox),
+                               float(tau), int(k0), int(k1), _p(L), _p(post), _p(bits),
+                               int(nthreads))
     return dict(L=L, post=post, bits=bits)
 
 
@@ -253,17 +328,21 @@ def color(P, W, H, grid, frames, mu, sigma, vox, slm_gate=0.5, sigma_floor=1.0, 
 
 def train_background(frames, sigma_floor=1.0):
     """NEXT-3: per-pixel, per-channel mean and population standard
-    deviation of a list of [H, W, 3] uint8 frames, sigma clamped to the floor.
-    Returns (mean, sigma) float64 [H, W, 3]."""
+    deviation of a list of [H, W, nch] uint8 frames (nch = 3 RGB, 1 grayscale),
+    sigma clamped to the floor.  Returns (mean, sigma) float64 [H, W, nch]."""
     fr = [np.ascontiguousarray(f, np.uint8) for f in frames]
     if not fr:
         raise ValueError("EmptyInput")
     if any(f.shape != fr[0].shape for f in fr):
         raise ValueError("DimensionMismatch")
-    npx = fr[0].size // 3
     mean = np.empty(fr[0].shape, np.float64)
     sd = np.empty(fr[0].shape, np.float64)
-    lib().oracle_train_background(len(fr), npx, _p(_ptrs(fr)), float(sigma_floor), _p(mean), _p(sd))
+    if fr[0].shape[-1] == 3:
+        lib().oracle_train_background(len(fr), fr[0].size // 3, _p(_ptrs(fr)), float(sigma_floor),
+                                      _p(mean), _p(sd))
+    else:
+        lib().oracle_train_background_elems(len(fr), fr[0].size, _p(_ptrs(fr)), float(sigma_floor),
+                                            _p(mean), _p(sd))
     return mean, sd
 
 

@@ -437,10 +437,10 @@ void oracle_color(const oracle_rig *rig, const oracle_grid *g, const uint8_t *co
 /* the population standard deviation, sigma clamped up to the floor   */
 /* (R#6).  Two passes in double.                                       */
 /* ------------------------------------------------------------------------ */
-void oracle_train_background(int n, int64_t npx, const uint8_t *const *frames, double sigma_floor,
-                             double *mean_out, double *sigma_out)
+void oracle_train_background_elems(int n, int64_t nelem, const uint8_t *const *frames,
+                                   double sigma_floor, double *mean_out, double *sigma_out)
 {
-    for (int64_t e = 0; e < 3 * npx; ++e) {
+    for (int64_t e = 0; e < nelem; ++e) {
         double sum = 0.0;
         for (int f = 0; f < n; ++f) sum += (double)frames[f][e];
         const double mean = sum / n;
@@ -456,6 +456,13 @@ void oracle_train_background(int n, int64_t npx, const uint8_t *const *frames, d
     }
 }
 
+/* RGB frames: 3 elements per pixel. */
+void oracle_train_background(int n, int64_t npx, const uint8_t *const *frames, double sigma_floor,
+                             double *mean_out, double *sigma_out)
+{
+    oracle_train_background_elems(n, 3 * npx, frames, sigma_floor, mean_out, sigma_out);
+}
+
 int oracle_max_threads(void)
 {
 #ifdef _OPENMP
@@ -463,4 +470,145 @@ int oracle_max_threads(void)
 #else
     return 1;
 #endif
+}
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-3 boundary variants (R#25-R#27).    */
+/* ------------------------------------------------------------------------ */
+
+/* Grayscale input (and any channel count nch): Eq (1)-(2) with the single
+ * Gaussian of P:77 over nch independent 8-bit channels and the uniform
+ * foreground density over the 8-bit cube of that dimension, U = 256^-nch
+ * (S:134 fixes 256^-3 for RGB; grayscale is nch = 1, U = 256^-1, R#25), then
+ * Eq (5)-(9) as oracle_pixel.  For nch = 3 this is oracle_pixel term for term
+ * (tested bit for bit). */
+void oracle_pixel_nch(int nch, const uint8_t *I, const float *mu, const float *sigma,
+                      double sigma_floor, double p_occ,
+                      double *slm_out, double *lnp1_out, double *lnp0_out)
+{
+    double ln_g = 0.0; /* ln P(I|F=0) = sum_ch ln N(I_ch | mu_ch, sigma'_ch) */
+    for (int ch = 0; ch < nch; ++ch) {
+        double s = (double)sigma[ch];
+        if (s < sigma_floor) s = sigma_floor; /* sigma floor (R#6) */
+        ln_g += ln_gauss((double)I[ch], (double)mu[ch], s);
+    }
+    const double ln_u = -(double)nch * log(256.0);   /* ln U, U = 256^-nch (R#25) */
+    const double ln_fg = ln_u + log(0.5);             /* ln P(I|F=1)P(F=1) */
+    const double ln_bg = ln_g + log(0.5);             /* ln P(I|F=0)P(F=0) */
+    const double dd = ln_bg - ln_fg;
+    const double slm = 1.0 / (1.0 + exp(dd));
+    const double one_minus_slm = 1.0 / (1.0 + exp(-dd));
+    const double p_o1 = p_occ, p_o0 = 1.0 - p_occ;
+    const double p_s_v1 = p_o0 * slm /* Eq 8 */ + p_o1 * slm /* Eq 9 */;
+    const double p_s_v0 = p_o0 * one_minus_slm /* Eq 6 */ + p_o1 * slm /* Eq 7 */;
+    if (slm_out) *slm_out = slm;
+    if (lnp1_out) *lnp1_out = log(p_s_v1);
+    if (lnp0_out) *lnp0_out = log(p_s_v0);
+}
+
+void oracle_slm_image_nch(int nch, int64_t n, const uint8_t *img, const float *mu,
+                          const float *sigma, double sigma_floor, double p_occ, double *slm,
+                          double *lnp1, double *lnp0, int nthreads)
+{
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1)
+#endif
+    for (int64_t p = 0; p < n; ++p) {
+        oracle_pixel_nch(nch, img + (int64_t)nch * p, mu + (int64_t)nch * p, sigma + (int64_t)nch * p,
+                         sigma_floor, p_occ, slm ? slm + p : NULL, lnp1 ? lnp1 + p : NULL,
+                         lnp0 ? lnp0 + p : NULL);
+    }
+    (void)nthreads;
+}
+
+/* The pinned projection's continuous coordinates: the float operations of
+ * oracle_project_pinned, returning u = RN(x'/w), v = RN(y'/w) (the +1/2 of
+ * round-half-up folded in, so u - 1/2 is the voxel centre's continuous pixel
+ * x coordinate, pixel centres at integers, R#11) and the same in-view
+ * decision (w > 0 and the nearest pixel inside the image, R#12, R#26). */
+int oracle_project_pinned_uv(const float A[12], int W, int H, int i, int j, int k,
+                             float *u_out, float *v_out)
+{
+    const float fi = (float)i, fj = (float)j, fk = (float)k;
+    const float x = fmaf(A[2], fk, fmaf(A[1], fj, fmaf(A[0], fi, A[3])));
+    const float y = fmaf(A[6], fk, fmaf(A[5], fj, fmaf(A[4], fi, A[7])));
+    const float w = fmaf(A[10], fk, fmaf(A[9], fj, fmaf(A[8], fi, A[11])));
+    if (!(w > 0.0f)) return 0;
+    const float rr = 1.0f / w;
+    const float u = x * rr;
+    const float v = y * rr;
+    if (!(u >= 0.0f && u < (float)W && v >= 0.0f && v < (float)H)) return 0;
+    *u_out = u;
+    *v_out = v;
+    return 1;
+}
+
+static int clampi(int a, int lo, int hi) { return a < lo ? lo : (a > hi ? hi : a); }
+
+/* Bilinear sample of a W x H double image at the continuous pixel position
+ * (x, y) (pixel centres at integers): the four pixel centres around it,
+ * x0 = floor(x), y0 = floor(y), weights (1-fx)(1-fy), fx(1-fy), (1-fx)fy, fx fy
+ * with fx = x - x0, fy = y - y0; neighbour indices clamped to the image
+ * ("bilinear SLM sampling at continuous projections, clamped at image
+ * borders"; R#26). */
+double oracle_bilinear(const double *img, int W, int H, double x, double y)
+{
+    const double x0 = floor(x), y0 = floor(y);
+    const double fx = x - x0, fy = y - y0;
+    const int xa = clampi((int)x0, 0, W - 1), xb = clampi((int)x0 + 1, 0, W - 1);
+    const int ya = clampi((int)y0, 0, H - 1), yb = clampi((int)y0 + 1, 0, H - 1);
+    const double s00 = img[(int64_t)ya * W + xa], s10 = img[(int64_t)ya * W + xb];
+    const double s01 = img[(int64_t)yb * W + xa], s11 = img[(int64_t)yb * W + xb];
+    return (1.0 - fx) * (1.0 - fy) * s00 + fx * (1.0 - fy) * s10 + (1.0 - fx) * fy * s01 +
+           fx * fy * s11;
+}
+
+/* Eq (3)-(4) + threshold with the bilinear SLM sample of
+ * every in-view camera (R#26): SLM_s = oracle_bilinear(SLM_c, u - 1/2,
+ * v - 1/2), then the per-view likelihoods of Eq (5)-(9) of that value
+ * (oracle_view_likelihood); out-of-view views contribute SLM = 1/2 (R#12).
+ * slm: per camera W x H double SLM images (oracle_slm_image). */
+void oracle_fuse_bilinear(const oracle_rig *rig, const oracle_grid *g, const double *const *slm,
+                          double p_vox, double tau, int k0, int k1, double *L_out,
+                          double *post_out, uint32_t *bits_out, int nthreads)
+{
+    const int64_t plane = (int64_t)g->xlen * g->ylen;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
+#endif
+    for (int k = k0; k < k1; ++k) {
+        for (int j = 0; j < g->ylen; ++j) {
+            for (int i = 0; i < g->xlen; ++i) {
+                double s1 = 0.0, s0 = 0.0, h1, h0;
+                oracle_view_likelihood(0.5, rig->p_occ, &h1, &h0);
+                for (int c = 0; c < rig->ncam; ++c) {
+                    float u, v;
+                    if (oracle_project_pinned_uv(rig->A + 12 * c, rig->W[c], rig->H[c], i, j, k, &u, &v)) {
+                        const double s = oracle_bilinear(slm[c], rig->W[c], rig->H[c],
+                                                         (double)u - 0.5, (double)v - 0.5);
+                        double l1, l0;
+                        oracle_view_likelihood(s, rig->p_occ, &l1, &l0);
+                        s1 += l1;
+                        s0 += l0;
+                    } else {
+                        s1 += h1;
+                        s0 += h0;
+                    }
+                }
+                const double a1 = s1 + log(p_vox), a0 = s0 + log(1.0 - p_vox);
+                const int64_t v = (int64_t)i + (int64_t)g->xlen * (j + (int64_t)g->ylen * k);
+                const int64_t o = v - plane * k0;
+                const double post = posterior_from_logs(a1, a0);
+                if (L_out) L_out[o] = a1 - a0;
+                if (post_out) post_out[o] = post;
+                if (bits_out && post > tau) {
+#ifdef _OPENMP
+#pragma omp atomic
+#endif
+                    bits_out[o >> 5] |= 1u << (o & 31);
+                }
+            }
+        }
+    }
+    (void)nthreads;
 }

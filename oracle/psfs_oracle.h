@@ -49,6 +49,20 @@ void oracle_color(const oracle_rig *rig, const oracle_grid *g, const uint8_t *co
                   int32_t *count_out, double *margin_out);
 void oracle_train_background(int n, int64_t npx, const uint8_t *const *frames, double sigma_floor,
                              double *mean_out, double *sigma_out);
+void oracle_train_background_elems(int n, int64_t nelem, const uint8_t *const *frames,
+                                   double sigma_floor, double *mean_out, double *sigma_out);
+/* NEXT-3 variants */
+void oracle_pixel_nch(int nch, const uint8_t *I, const float *mu, const float *sigma,
+                      double sigma_floor, double p_occ, double *slm, double *lnp1, double *lnp0);
+void oracle_slm_image_nch(int nch, int64_t n, const uint8_t *img, const float *mu,
+                          const float *sigma, double sigma_floor, double p_occ, double *slm,
+                          double *lnp1, double *lnp0, int nthreads);
+int oracle_project_pinned_uv(const float A[12], int W, int H, int i, int j, int k, float *u,
+                             float *v);
+double oracle_bilinear(const double *img, int W, int H, double x, double y);
+void oracle_fuse_bilinear(const oracle_rig *rig, const oracle_grid *g, const double *const *slm,
+                          double p_vox, double tau, int k0, int k1, double *L_out,
+                          double *post_out, uint32_t *bits_out, int nthreads);
 int oracle_max_threads(void);
 
 #endif

@@ -72,8 +72,8 @@ class Scene:
     name: str
     grid: Grid
     cameras: list
-    mu: np.ndarray      # float32 [ncam, H, W, 3]
-    sigma: np.ndarray   # float32 [ncam, H, W, 3]
+    mu: np.ndarray      # float32 [ncam, H, W, nch] (nch = 3 RGB, 1 grayscale)
+    sigma: np.ndarray   # float32 [ncam, H, W, nch]
     seed: int
     body: str = "skeleton"
     fg_noise: float = 6.0
@@ -82,6 +82,10 @@ class Scene:
     @property
     def ncam(self) -> int:
         return len(self.cameras)
+
+    @property
+    def channels(self) -> int:
+        return int(self.mu.shape[-1])
 
     @property
     def P(self) -> np.ndarray:
@@ -179,12 +183,13 @@ def _rng(seed: int, *stream) -> np.random.Generator:
 
 
 def make_background(seed, cam, W, H, sigma_range=(2.0, 8.0), integer_mu=False,
-                    const_sigma=None):
-    """mu: smooth random field in [20, 235]; sigma: uniform in sigma_range."""
+                    const_sigma=None, channels=3):
+    """mu: smooth random field in [20, 235]; sigma: uniform in sigma_range.
+    channels: 3 (RGB) or 1 (grayscale, NEXT-3)."""
     rng = _rng(seed, 1, cam)
     y, x = np.mgrid[0:H, 0:W].astype(np.float32)
-    mu = np.empty((H, W, 3), np.float32)
-    for ch in range(3):
+    mu = np.empty((H, W, channels), np.float32)
+    for ch in range(channels):
         a = rng.uniform(0.5, 2.5, size=4)
         ph = rng.uniform(0, 2 * np.pi, size=4)
         field_ = (60.0 * np.sin(2 * np.pi * (a[0] * x / W + a[1] * y / H) + ph[0])
@@ -194,9 +199,9 @@ def make_background(seed, cam, W, H, sigma_range=(2.0, 8.0), integer_mu=False,
     if integer_mu:
         mu = np.round(mu).astype(np.float32)
     if const_sigma is not None:
-        sigma = np.full((H, W, 3), const_sigma, np.float32)
+        sigma = np.full((H, W, channels), const_sigma, np.float32)
     else:
-        sigma = rng.uniform(sigma_range[0], sigma_range[1], size=(H, W, 3)).astype(np.float32)
+        sigma = rng.uniform(sigma_range[0], sigma_range[1], size=(H, W, channels)).astype(np.float32)
     return mu, sigma
 
 
@@ -370,13 +375,15 @@ def render_silhouette(cam: Camera, parts) -> np.ndarray:
 
 def _noisy_frame(seed, frame, cam_idx, mu, sigma, labels, fg_noise):
     rng = _rng(seed, 2, frame, cam_idx)
-    H, W, _ = mu.shape
-    n_bg = rng.standard_normal((H, W, 3), dtype=np.float32)
+    H, W, nch = mu.shape
+    n_bg = rng.standard_normal((H, W, nch), dtype=np.float32)
     img = mu + sigma * n_bg
     fg = labels >= 0
     if fg.any():
-        n_fg = rng.standard_normal((int(fg.sum()), 3), dtype=np.float32)
+        n_fg = rng.standard_normal((int(fg.sum()), nch), dtype=np.float32)
         cols = PALETTE[labels[fg] % len(PALETTE)]
+        if nch != 3:  # grayscale: the palette colour's channel mean
+            cols = cols.mean(axis=1, keepdims=True)
         img[fg] = cols + fg_noise * n_fg
     return np.clip(np.rint(img), 0, 255).astype(np.uint8)
 
@@ -410,7 +417,7 @@ def body_parts(body: str, frame: int, fps: float = 30.0, motion: bool = False):
 
 def make_frames(scene: Scene, frame: int, mode: str = "noisy", motion: bool = False,
                 labels_out: list | None = None) -> np.ndarray:
-    """uint8 [ncam, H, W, 3] RGB frame set for one time step."""
+    """uint8 [ncam, H, W, nch] frame set for one time step (RGB or grayscale)."""
     parts = body_parts(scene.body, frame, motion=motion)
     out = []
     for c, cam in enumerate(scene.cameras):
@@ -432,7 +439,9 @@ def make_frames(scene: Scene, frame: int, mode: str = "noisy", motion: bool = Fa
 
 def make_scene(name: str = "C1", body: str = "skeleton", seed: int | None = None,
                grid: Grid | None = None, integer_mu: bool = False, const_sigma=None,
-               rings=None, W=None, H=None) -> Scene:
+               rings=None, W=None, H=None, channels: int = 3) -> Scene:
+    """channels: 3 (8-bit RGB, the default) or 1 (8-bit grayscale, NEXT-3):
+    mu / sigma / frames carry that many channels in their last axis."""
     cfg = CONFIGS[name]
     seed = config_seed(name) if seed is None else seed
     grid = grid or cube_grid(cfg["n"])
@@ -442,7 +451,7 @@ def make_scene(name: str = "C1", body: str = "skeleton", seed: int | None = None
     mus, sigs = [], []
     for c, cam in enumerate(cams):
         mu, sg = make_background(seed, c, cam.width, cam.height, integer_mu=integer_mu,
-                                 const_sigma=const_sigma)
+                                 const_sigma=const_sigma, channels=channels)
         mus.append(mu)
         sigs.append(sg)
     return Scene(name=name, grid=grid, cameras=cams, mu=np.stack(mus), sigma=np.stack(sigs),

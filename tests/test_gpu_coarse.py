@@ -167,6 +167,11 @@ def test_zslab_handles(world):
         w0, w1 = plane * rec.k0 // 32, plane * rec.k1 // 32
         out[:, w0:w1] = B[:, w0:w1]
     assert torch.equal(out, full)
+    # the assembled slabs against the oracle, every frame
+    Bh = out.cpu().numpy().view(np.uint32)
+    for f in range(nf):
+        orc = oracle.scene_reconstruct(s, make_frames(s, f), nthreads=NTHREADS)
+        assert_parity(None, Bh[f], orc, s.grid.nvox)
 
 
 @pytest.mark.parametrize("dims,coarse", [((37, 29, 23), False), ((64, 29, 23), True),

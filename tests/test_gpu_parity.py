@@ -255,6 +255,9 @@ def test_zslab_handles_concatenate_to_full(world):
         roi = part["rec"].roi()
         assert ((roi[:, 1] - roi[:, 0]) <= (roi_full[:, 1] - roi_full[:, 0])).all()
     assert np.array_equal(bits, full["bits"][0])
+    # the assembled slabs against the oracle (A5 parity)
+    orc = oracle.scene_reconstruct(s, fr[0], nthreads=NTHREADS)
+    assert_parity(None, bits, orc, s.grid.nvox)
 
 
 def test_reconstruct_host_matches_device_path():
@@ -314,17 +317,21 @@ def test_full_size_sampled(name):
 
 @pytest.mark.parametrize("name,with_logodds", [("C4", True), ("C5", False)])
 def test_full_size_sixteen_frame_pass(name, with_logodds):
-    """The full-size configurations in bench.py's launch configuration: one
-    16-frame pass (k_voxel16, NCAM = 16 for C4, the generic camera loop for
-    C5's 32 cameras) over 2 distinct frame sets repeated 8 times; both distinct
-    frames checked on the voxel sample against the oracle (log-odds for C4,
-    bits for C5, whose 16 log-odds volumes would need 64 GB), and every repeat
-    bit-identical to its original."""
+    """The full-size configurations through the exact path's 16-frame pass
+    (k_likelihood halves + k_voxel16: NCAM = 16 for C4, the generic camera loop
+    k_voxel16<0> for C5's 32 cameras) over 2 distinct frame sets repeated 8
+    times.  Coarse passes are switched off (psfs_set_coarse(0)) so the bits-only
+    C5 call takes the exact kernels too.  Both distinct frames are checked on
+    the voxel sample against the oracle (log-odds for C4, bits for both; C5's
+    16 log-odds volumes would need 64 GB), and every repeat is bit-identical to
+    its original."""
     from paper_1311_6811_b200 import from_scene
     s = make_scene(name)
     two = [make_frames(s, 0), make_frames(s, 1)]
     fr = torch.from_numpy(np.stack(two)).cuda().repeat(8, 1, 1, 1, 1)
     rec = from_scene(s)
+    rec.set_coarse(0)
+    assert not rec.coarse_status()[0]
     L, B = rec.alloc_outputs(16, logodds=with_logodds)
     rec.reconstruct_batch(fr, 16, logodds=L, bits=B)
     torch.cuda.synchronize()

@@ -3,8 +3,12 @@ psfs_reconstruct_peer) with real CUDA IPC mappings:
 `world` processes share GPU 0 (one process per rank, exactly as one process
 per GPU, only the peer stores stay on one device), torch.distributed (gloo)
 moves the IPC handles once, stage 2 stores every slab byte into every rank's
-buffer and device-side barriers order the exchange.  Every rank must end up
-with the single-handle full-grid bitmask, bit for bit."""
+buffer and device-side barriers order the exchange.  Every rank's assembled
+full-grid bitmask is checked against the CPU oracle frame by frame (bits exact
+outside the 1e-4 posterior band; BASELINE.json north_star), and against the
+single-handle run bit for bit.  The all-gather variant (peer=False) runs the
+same slab handles with the words gathered by parallel.allgather_bits (gloo on
+CPU tensors here: NCCL refuses two ranks on one device)."""
 import os
 import socket
 
@@ -14,8 +18,11 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+import oracle
 from synth.scene import Grid, make_frames, make_scene
-from tests.helpers import gpu_run
+from tests.helpers import assert_parity, gpu_run
+
+NTHREADS = max(1, len(os.sched_getaffinity(0)))
 
 pytestmark = pytest.mark.gpu
 
@@ -45,8 +52,22 @@ def _worker(rank, world, port, kind, nframes, mode, q):
         from paper_1311_6811_b200.parallel import ZSlabReconstructor
         torch.cuda.set_device(0)
         s = _scene(kind)
-        z = ZSlabReconstructor(s, rank=rank, world=world, device=0, peer=True, max_frames=nframes)
+        z = ZSlabReconstructor(s, rank=rank, world=world, device=0, peer=(mode != "allgather"),
+                               max_frames=nframes)
         fr = torch.from_numpy(np.stack([make_frames(s, f) for f in range(nframes)])).cuda()
+        if mode == "allgather":
+            from paper_1311_6811_b200.parallel import allgather_bits
+            out = []
+            for lo in (False, True):  # bits only (coarse passes when >= 16 frames) / with log-odds (exact)
+                L, B = z.rec.alloc_outputs(nframes, logodds=lo)
+                z.reconstruct_batch(fr, nframes, logodds=L, bits=B, gather=False)
+                torch.cuda.synchronize()
+                Bc = B.cpu()
+                g = s.grid
+                allgather_bits(Bc, g.xlen, g.ylen, g.zlen, world, rank)
+                out.append(Bc.numpy().copy())
+            q.put((rank, out))
+            return
         if mode == "timeout":
             # rank 1 never enters the exchange: rank 0's barriers must give up
             # (bounded spin) and report PSFS_ETIMEOUT instead of hanging
@@ -86,16 +107,40 @@ def _run(world, kind, nframes, mode="ok"):
     return res
 
 
+def _oracle_bits_check(s, frames, words_per_frame):
+    """Every frame's full-grid bitmask against the oracle (A5 parity)."""
+    for f, fr in enumerate(frames):
+        orc = oracle.scene_reconstruct(s, fr, nthreads=NTHREADS)
+        assert_parity(None, words_per_frame[f], orc, s.grid.nvox)
+
+
 @pytest.mark.parametrize("world,kind,nframes", [(2, "C1", 3), (4, "C1", 17), (2, "ragged", 2)])
 def test_fused_exchange_gives_every_rank_the_full_grid(world, kind, nframes):
+    """3 frames: exact path; 17 frames on C1: one coarse pass with the fix-up
+    patching every rank's buffer; ragged rows: atomic ORs into peer words."""
     res = _run(world, kind, nframes)
     s = _scene(kind)
     frames = [make_frames(s, f) for f in range(nframes)]
     ref = gpu_run(s, frames, fuse=16)["bits"]
     ref_flip = ref[::-1]
     for r in range(world):
-        assert np.array_equal(res[r][0].view(np.uint32), ref), r
+        got = res[r][0].view(np.uint32)
+        _oracle_bits_check(s, frames, got)
+        _oracle_bits_check(s, frames[::-1], res[r][1].view(np.uint32))
+        assert np.array_equal(got, ref), r
         assert np.array_equal(res[r][1].view(np.uint32), ref_flip), r
+
+
+@pytest.mark.parametrize("world,nframes", [(2, 3), (4, 17)])
+def test_allgather_exchange_against_oracle(world, nframes):
+    """The all-gather variant of the z-slab exchange: every rank's gathered
+    bitmask (bits-only call and log-odds call) against the oracle."""
+    res = _run(world, "C1", nframes, mode="allgather")
+    s = _scene("C1")
+    frames = [make_frames(s, f) for f in range(nframes)]
+    for r in range(world):
+        for out in res[r]:
+            _oracle_bits_check(s, frames, out.view(np.uint32))
 
 
 def test_barrier_times_out_instead_of_hanging():
