@@ -67,6 +67,8 @@ enum {
 #define PSFS_MAX_PEERS 8    /* ranks of one fused peer exchange (one node) */
 #define PSFS_MAX_TRAIN_FRAMES 512 /* frames of one psfs_train_background call */
 #define PSFS_IPC_HANDLE_BYTES 64 /* size of one exported peer buffer handle */
+#define PSFS_SAMPLE_NEAREST 0  /* the pixel nearest the projected voxel centre (R#10) */
+#define PSFS_SAMPLE_BILINEAR 1 /* bilinear SLM sample, clamped at the borders (R#26) */
 
 typedef struct psfs_handle psfs_handle; /* opaque, library-owned */
 
@@ -118,9 +120,25 @@ int psfs_create(const psfs_grid *grid, const psfs_params *params, const psfs_dis
 int psfs_set_cameras(psfs_handle *h, int32_t ncam, const double *P, const int32_t *width,
                      const int32_t *height);
 
+/* NEXT-3 boundary variants, any time after psfs_create:
+ * channels = 3: 8-bit RGB frames (default; U = 256^-3); channels = 1:
+ * 8-bit grayscale frames, H*W bytes per image, single-channel background
+ * models, U = 256^-1 (R#25).  Changing the channel count discards every
+ * background model (set or train them again before reconstructing).
+ * sampling = PSFS_SAMPLE_NEAREST (default, the hot path) or
+ * PSFS_SAMPLE_BILINEAR: each in-view camera contributes the per-view term of
+ * Eq 5-9 evaluated at the bilinear interpolation of its SLM image
+ * (Eq 1-2) around the projected voxel centre, neighbours clamped to the image
+ * (R#26); the in-view rule is the nearest-pixel one (R#12).  Coarse
+ * passes apply only to RGB nearest-pixel handles; other combinations take the
+ * exact path (bilinear: groups of <= 8 frames).  psfs_color needs RGB.
+ * Errors: PSFS_EINVAL (other values). */
+int psfs_set_input(psfs_handle *h, int32_t channels, int32_t sampling);
+
 /* Set camera `cam`'s single-Gaussian background model: mean and sigma
- * (a standard deviation per channel, R#2), HOST, height*width*3 floats each,
- * row-major, channel-interleaved (the frame layout).  sigma is clamped to
+ * (a standard deviation per channel, R#2), HOST, height*width*channels floats
+ * each (channels of psfs_set_input, default 3), row-major, channel-interleaved
+ * (the frame layout).  sigma is clamped to
  * sigma_floor (R#6).  Errors: PSFS_ESTATE (no cameras), PSFS_EINVAL (cam out
  * of range, NULL, non-finite values), PSFS_EDIM (width/height differ from the
  * camera's), PSFS_ECUDA. */
@@ -131,8 +149,8 @@ int psfs_set_background(psfs_handle *h, int32_t cam, int32_t width, int32_t heig
  * Gaussian of P:77 exists): camera `cam`'s per-pixel, per-channel sample mean
  * and population standard deviation over nframes background frames, sigma
  * clamped up to sigma_floor (R#6).  frames: HOST array of nframes
- * DEVICE pointers, each an H_c*W_c*3 uint8 image.  mean / sigma: DEVICE,
- * nullable, H_c*W_c*3 float (sigma after the clamp).  install != 0 makes the
+ * DEVICE pointers, each an H_c*W_c*channels uint8 image.  mean / sigma:
+ * DEVICE, nullable, H_c*W_c*channels float (sigma after the clamp).  install != 0 makes the
  * result camera cam's background model, exactly as psfs_set_background with
  * these float values would, without a host round trip.  Asynchronous on
  * cuda_stream.  Errors: PSFS_ESTATE (no cameras), PSFS_EINVAL (cam out of
@@ -143,7 +161,8 @@ int psfs_train_background(psfs_handle *h, int32_t cam, int32_t nframes,
                           void *cuda_stream);
 
 /* Reconstruct one frame set.  frames: HOST array of ncam DEVICE pointers, each
- * an H_c*W_c*3 uint8 RGB image (row-major, channel-interleaved).
+ * an H_c*W_c*3 uint8 RGB image (row-major, channel-interleaved; H_c*W_c bytes
+ * for a grayscale handle, psfs_set_input).
  * logodds: DEVICE, nullable, float per voxel of this handle's slab
  * (xlen*ylen*(k1-k0), x-fastest, slab-relative).  bits: DEVICE, nullable,
  * ceil(xlen*ylen*zlen/32) uint32 words for the FULL grid; this handle writes

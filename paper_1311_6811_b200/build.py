@@ -8,8 +8,10 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libpsfs.so")
-SOURCES = [os.path.join(HERE, "csrc", "psfs_api.cu"), os.path.join(HERE, "csrc", "psfs_kernels.cu")]
-DEPS = SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.h")) + [os.path.join(ROOT, "include", "psfs.h")]
+SOURCES = [os.path.join(HERE, "csrc", "psfs_api.cu"), os.path.join(HERE, "csrc", "psfs_kernels.cu"),
+           os.path.join(HERE, "csrc", "psfs_next3.cu")]
+DEPS = SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.h")) + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + \
+    [os.path.join(ROOT, "include", "psfs.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -98,6 +98,7 @@ struct VParams {
     float *lo_base;            // logodds[0] (nullable)
     int64_t lo_stride;         // floats per frame
     int32_t word_rows;         // xlen % 32 == 0: a 32-wide tile row is one bitmask word
+    float bl_a, bl_b;          // bilinear sampling (k_voxel_bl): 1 - p_O, 2 p_O - 1
 };
 
 // ---- coarse passes (bits-only calls) -------------------
@@ -191,6 +192,7 @@ struct H2DParams {
     int32_t W[kMaxCam], r0[kMaxCam], c0[kMaxCam], ncol[kMaxCam];
     int32_t task_begin[kMaxCam + 1];      // row tasks of camera c in one frame: [task_begin[c], task_begin[c+1])
     int32_t nf, ncam;
+    int32_t bpp;      // bytes per pixel (3 RGB, 1 grayscale)
     int32_t aligned;  // 16: every image and staging image 16-byte aligned with a whole number of
                       // 16-byte chunks (chunked copy); 4: every row segment 4-byte aligned; 1: bytes
 };
@@ -232,6 +234,11 @@ struct PeerBarrier {
 
 // Launchers (psfs_kernels.cu).  Return the cudaError_t of the launch.
 cudaError_t launch_likelihood(const S1Params &p, int F, int max_roi_px, int path, cudaStream_t s);
+// NEXT-3 (psfs_next3.cu): stage 1 for nch-byte pixels (1 grayscale, 3 RGB), storing
+// the Q11.20 term (slm = false) or the float SLM (slm = true, bilinear sampling);
+// F in {1, 2, 4, 8, 16}.  Stage 2 with bilinear SLM samples, F in {1, 2, 4, 8}.
+cudaError_t launch_s1x(const S1Params &p, int F, int nch, bool slm, int max_roi_px, cudaStream_t s);
+cudaError_t launch_voxel_bl(const VParams &p, int F, cudaStream_t s);
 cudaError_t launch_prep_model(ModelPx *model, int64_t begin, int64_t n, double c0, cudaStream_t s);
 // NEXT-3 background training (psfs_train_background): up to kMaxTrain frame
 // pointers travel in the kernel parameters (no device table, no sync).
@@ -241,6 +248,7 @@ struct TrainParams {
     int32_t n;
     int64_t nelem;     // 3 * W * H
     float floor_f;
+    int32_t nch;       // channels per pixel (3 RGB, 1 grayscale)
     float *mean, *sigma;
     ModelPx *model;    // non-null: install (mu, sigma') into these records
 };

@@ -40,7 +40,10 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_set_carve", "psfs_surface", "psfs_smooth_threshold", "psfs_peer_alloc",
            "psfs_peer_open", "psfs_reconstruct_peer", "psfs_peer_status", "psfs_color",
            "psfs_train_background", "psfs_probe_gather_bandwidth", "psfs_set_coarse",
-           "psfs_coarse_plan", "psfs_coarse_status", "psfs_debug_codes", "psfs_set_host_upload"]
+           "psfs_coarse_plan", "psfs_coarse_status", "psfs_debug_codes", "psfs_set_host_upload",
+           "psfs_set_input"]
+SAMPLE_NEAREST = 0
+SAMPLE_BILINEAR = 1
 MAX_COARSE = 64
 
 
@@ -120,6 +123,7 @@ def lib():
         L.psfs_coarse_status.argtypes = [vp, C.POINTER(i32), C.POINTER(C.c_int64), i32]
         L.psfs_debug_codes.argtypes = [vp, vp, vp, vp]
         L.psfs_set_host_upload.argtypes = [vp, i32]
+        L.psfs_set_input.argtypes = [vp, i32, i32]
         _lib = L
     return _lib
 
@@ -211,6 +215,8 @@ class Reconstructor:
         self.k0, self.k1 = k0.value, k1.value
         self.ncam = 0
         self.widths = self.heights = None
+        self.channels = 3
+        self.sampling = SAMPLE_NEAREST
 
     # -- lifecycle ---------------------------------------------------------
     def close(self):
@@ -240,11 +246,18 @@ class Reconstructor:
         self.widths, self.heights = W.copy(), H.copy()
         self.npix = int((W.astype(np.int64) * H).sum())
 
+    def set_input(self, channels: int = 3, sampling: int = SAMPLE_NEAREST):
+        """NEXT-3: 3 (RGB) or 1 (grayscale) channels per pixel; nearest-pixel or
+        bilinear SLM sampling (include/psfs.h psfs_set_input).  A channel change
+        discards the background models."""
+        self._check(lib().psfs_set_input(self._h, int(channels), int(sampling)), "psfs_set_input")
+        self.channels, self.sampling = int(channels), int(sampling)
+
     def set_background(self, cam, mean, sigma):
         mean = np.ascontiguousarray(np.asarray(mean, np.float32))
         sigma = np.ascontiguousarray(np.asarray(sigma, np.float32))
-        if mean.ndim != 3 or mean.shape != sigma.shape or mean.shape[2] != 3:
-            raise ValueError("mean/sigma must be [H, W, 3] float32")
+        if mean.ndim != 3 or mean.shape != sigma.shape or mean.shape[2] != self.channels:
+            raise ValueError(f"mean/sigma must be [H, W, {self.channels}] float32")
         self._check(lib().psfs_set_background(self._h, int(cam), mean.shape[1], mean.shape[0],
                                               mean.ctypes.data, sigma.ctypes.data),
                     "psfs_set_background")
@@ -256,7 +269,7 @@ class Reconstructor:
         import torch
         if not (isinstance(frames, torch.Tensor) and frames.is_cuda and frames.dtype == torch.uint8
                 and frames.is_contiguous() and frames.dim() == 4):
-            raise TypeError("frames must be a contiguous uint8 CUDA tensor [n, H, W, 3]")
+            raise TypeError("frames must be a contiguous uint8 CUDA tensor [n, H, W, channels]")
         n = frames.shape[0]
         per = frames[0].numel()
         ptrs = _ptr_array([frames.data_ptr() + f * per for f in range(n)])
@@ -438,7 +451,7 @@ class Reconstructor:
             assert x.flags["C_CONTIGUOUS"]
             return x.ctypes.data
         base = hp(frames_host)
-        per_cam = int(self.widths[0]) * int(self.heights[0]) * 3
+        per_cam = int(self.widths[0]) * int(self.heights[0]) * self.channels
         if not (self.widths == self.widths[0]).all() or not (self.heights == self.heights[0]).all():
             raise ValueError("reconstruct_host helper assumes equal camera sizes")
         ptrs = _ptr_array([base + i * per_cam for i in range(nframes * self.ncam)])
@@ -574,10 +587,13 @@ def probe_l1_bandwidth() -> float:
     return float(v.value)
 
 
-def from_scene(scene, params=None, device=None, rank=0, world=1) -> Reconstructor:
+def from_scene(scene, params=None, device=None, rank=0, world=1, sampling=SAMPLE_NEAREST) -> Reconstructor:
     """Build a Reconstructor for a synth.Scene-like object (grid, P, widths,
-    heights, mu, sigma)."""
+    heights, mu, sigma; the channel count is mu's last axis)."""
     r = Reconstructor(scene.grid, params, device, rank, world)
+    nch = int(np.asarray(scene.mu).shape[-1])
+    if nch != 3 or sampling != SAMPLE_NEAREST:
+        r.set_input(nch, sampling)
     r.set_cameras(scene.P, scene.widths, scene.heights)
     for c in range(scene.ncam):
         r.set_background(c, scene.mu[c], scene.sigma[c])
