@@ -250,12 +250,14 @@ int psfs_debug_roi(const psfs_handle *h, int32_t *out);
 /* Enable/disable the ROI restriction of stage 1 (default on). */
 int psfs_set_roi_enabled(psfs_handle *h, int32_t enabled);
 
-/* Stage-1 kernel: 0 = one pixel per thread (default); 1 = TMA bulk-copy ring
- * (needs every W % 16 == 0 and 16-byte aligned frames); 2 = software-pipelined
- * persistent kernel; 3 = four pixels per thread (W % 4, 4-byte aligned frames);
- * 4 = warp-row coalesced image loads with shuffles (W % 32, 4-byte aligned).
+/* Stage-1 kernel of the exact path: 0 = one pixel per thread; 1 = TMA
+ * bulk-copy ring (needs every W % 16 == 0 and 16-byte aligned frames); 2 =
+ * software-pipelined persistent kernel; 3 = four pixels per thread (W % 4,
+ * 4-byte aligned frames); 4 = warp-row coalesced image loads with shuffles (W %
+ * 32, 4-byte aligned); 5 = cp.async ring per warp; 6 = persistent four pixels
+ * per thread, whole pass per thread (W % 4, 4-byte aligned frames; default).
  * A path whose requirement fails falls back to 0.  All give bit-identical terms
- * (DESIGN.md §8 has the measurements that made 0 the default). */
+ * (DESIGN.md §8 has the measurements that made 6 the default). */
 int psfs_set_stage1_path(psfs_handle *h, int32_t path);
 
 /* Bits-only early exit (default off): when a call requests no log-odds, a

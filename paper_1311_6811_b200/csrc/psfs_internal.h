@@ -54,6 +54,7 @@ struct S1Params {
     int32_t nchunk;  // async path: 32-pixel row chunks over all cameras
     int32_t tf;      // frames per term record (the pass's F: 1..16)
     int32_t halves;  // 2: a 16-frame pass run as two 8-frame halves (path 0/4 only)
+    int32_t n4;      // path 6: 4-pixel groups over all cameras (cam[c].pad_[0] = camera c's first)
 };
 
 // Stage 2 (voxel) launch description.
@@ -99,6 +100,7 @@ struct VParams {
     int64_t lo_stride;         // floats per frame
     int32_t word_rows;         // xlen % 32 == 0: a 32-wide tile row is one bitmask word
     float bl_a, bl_b;          // bilinear sampling (k_voxel_bl): 1 - p_O, 2 p_O - 1
+    int32_t lo_pairs;          // k_voxel16: x-adjacent log-odds as 8-byte stores (xlen, lo_stride even, 8-B base)
 };
 
 // ---- coarse passes (bits-only calls) -------------------

@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(256) k_voxel_bl(const __grid_constant__ VParam
         for (int f = 0; f < F; ++f) {
             const unsigned m = __ballot_sync(0xffffffffu, valid && S[f] > p.Tq);
             if (p.lo_base && valid)
-                p.lo_base[f * p.lo_stride + o] = (float)((double)S[f] * (1.0 / kQ) + p.logit_pv);
+                p.lo_base[f * p.lo_stride + o] = logodds_of(S[f], p.logit_pv);
             if (lane == 0) {
                 if (p.npeer == 0) {
                     if (p.bits_base) p.bits_base[f * p.bits_stride + word] = m;

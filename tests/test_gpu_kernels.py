@@ -52,7 +52,7 @@ def test_camera_inside_grid_uses_exact_reciprocal_and_matches_oracle():
     assert_parity(g["L"][0], g["bits"][0], orc, s.grid.nvox)
 
 
-@pytest.mark.parametrize("path", [0, 2, 3, 4, 5])
+@pytest.mark.parametrize("path", [0, 2, 3, 4, 5, 6])
 def test_stage1_paths_bit_identical(path):
     """The three stage-1 kernels (TMA ring with cp.async.bulk + mbarrier, used
     when frames are 16-byte aligned and W % 16 == 0; pipelined persistent; one
@@ -83,7 +83,8 @@ def test_stage1_paths_bit_identical(path):
         assert torch.equal(r.debug_terms(aligned[0]), ref.debug_terms(shifted[0]))
 
 
-@pytest.mark.parametrize("path,ty,kz", [(0, 1, 1), (4, 1, 4), (0, 1, 16), (0, 4, 1), (4, 4, 3), (5, 1, 4)])
+@pytest.mark.parametrize("path,ty,kz", [(0, 1, 1), (4, 1, 4), (0, 1, 16), (0, 4, 1), (4, 4, 3), (5, 1, 4),
+                                        (6, 1, 4), (6, 4, 3)])
 def test_sixteen_frame_passes_bit_identical(path, ty, kz):
     """16-frame passes (stage 1 as two 8-frame halves, warp-row or one-pixel
     loads; k_voxel16 with lane pairs) equal 8-frame passes bit for bit, for
