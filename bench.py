@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--no-zslab", action="store_true", help="skip the C4 z-slab section")
     ap.add_argument("--zslab-frames", type=int, default=64, help="frame sets per z-slab call (even)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondaries", action="store_true",
+                    help="skip the full-output, NEXT-3 and other-config legs")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (1024^3, 32 cameras) leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true",
                     help="ncu mode: no clocks sampling / cpu baseline / e2e")
@@ -228,6 +231,27 @@ def cpu_baseline(scene, frames, seconds, nthreads):
     return n / el, n, el
 
 
+def cpu_info():
+    """CPU model and core counts of the host (lscpu; SURVEY.md 8(d) oracle timing)."""
+    info = {"logical_cpus": os.cpu_count(), "affinity_cpus": host_cores()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {}
+        for ln in out.splitlines():
+            if ":" in ln:
+                k, v = ln.split(":", 1)
+                kv[k.strip()] = v.strip()
+        info["model"] = kv.get("Model name")
+        tpc = int(kv.get("Thread(s) per core", "1") or 1)
+        cps = int(kv.get("Core(s) per socket", "0") or 0)
+        sockets = int(kv.get("Socket(s)", "1") or 1)
+        info["physical_cores"] = cps * sockets if cps else None
+        info["threads_per_core"] = tpc
+    except Exception as e:  # reported, not fatal
+        info["lscpu_error"] = str(e)[:100]
+    return info
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -297,6 +321,193 @@ def device_us(fn, dev, reps=20):
         e1.record(s)
     torch.cuda.synchronize(dev)
     return e0.elapsed_time(e1) / reps * 1e3
+
+
+def pct(xs, q):
+    return float(np.percentile(np.asarray(xs, dtype=np.float64), q))
+
+
+def step_stats(xs):
+    return {"median": statistics.median(xs), "p10": pct(xs, 10), "p90": pct(xs, 90), "min": min(xs),
+            "max": max(xs)}
+
+
+def timed_calls(fn, steps, stream, flush=None):
+    """Device time (ms) of each fn() call on `stream` between CUDA events, after
+    a synchronize; the L2 is flushed before each call (outside the events) when a
+    (write, read) buffer pair is given."""
+    import torch
+    out = []
+    for k in range(steps):
+        if flush is not None:
+            flush[0].fill_(k)
+            flush[1].sum()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn(k)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out.append(e0.elapsed_time(e1))
+    return out
+
+
+def max_over_ranks(ms, world, dev):
+    if world == 1:
+        return ms
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def roi_pixels(rec):
+    roi = rec.roi()
+    return int(((roi[:, 1] - roi[:, 0]).astype(np.int64) * (roi[:, 3] - roi[:, 2])).sum())
+
+
+def full_output_leg(args, scene, frames_dev, B, pool, dev, stream, flush, world, hbm_peak, gather_peak,
+                    hbm_src):
+    """The north star's whole output (Eq 3 log-odds, and the bitmask): the
+    same C2 step as the headline with log-odds requested, i.e. the exact int32
+    path (16-frame passes of k_likelihood_x4p + k_voxel16, stage 1 of pass g+1
+    overlapped with stage 2 of pass g), 8 MiB of float log-odds per frame.
+    Rooflines: stage 1 against HBM (algorithmic bytes = ROI px x (24 B model +
+    16 x (3 B image + 4 B term))), stage 2 against the binding one of the L2
+    gather (the live probe of its access pattern) and the HBM store of the
+    log-odds (nvox x 16 x 4 B per launch)."""
+    import torch
+    from paper_1311_6811_b200 import from_scene
+    rec = from_scene(scene, device=dev.index)
+    L, Bits = rec.alloc_outputs(B)
+
+    tabs = [rec.frame_pointers(frames_dev[i0:i0 + B], B) for i0 in range(0, pool - B + 1, B)]
+
+    def step(k):
+        rec.reconstruct_batch(tabs[k % len(tabs)], B, logodds=L, bits=Bits, stream=stream)
+
+    for k in range(3):
+        step(k)
+    torch.cuda.synchronize(dev)
+    rec.set_profiling(True)
+    rec.kernel_times(reset=True)
+    ms = timed_calls(step, args.steps, stream, flush)
+    kt = rec.kernel_times(reset=True)
+    launches = rec.last_launch_count
+    rec.set_profiling(False)
+    total = max_over_ranks(sum(ms), world, dev)
+    F = 16
+    roi_px = roi_pixels(rec)
+    l_ms, l_n = kt["k_likelihood"]
+    v_ms, v_n = kt["k_voxel"]
+    s1_bytes = roi_px * (24 + 7 * F)
+    s1_t = (l_ms / max(l_n, 1)) / 1e3
+    lines, wf = gather_sectors(scene, F)
+    g_bytes = lines * wf
+    st_bytes = scene.grid.nvox * F * 4
+    v_t = (v_ms / max(v_n, 1)) / 1e3
+    t_gather = g_bytes / (gather_peak * 1e9) if gather_peak else None
+    t_store = st_bytes / (hbm_peak * 1e9)
+    bound_t = max(t_gather or 0.0, t_store)
+    out = {
+        "value": world * B * args.steps / (total / 1e3), "unit": "frames/s",
+        "ms_per_step": total / args.steps, "step_ms": step_stats(ms),
+        "voxel_camera_projections_per_s": world * B * args.steps / (total / 1e3) * scene.grid.nvox * scene.ncam,
+        "outputs": "float32 log-odds (8 MiB/frame) + occupancy bitmask (256 KiB/frame)",
+        "path": "exact int32 terms, 16-frame passes, stage 1 of pass g+1 beside stage 2 of pass g",
+        "launches_per_step": launches,
+        "stage1": {"kernel": "k_likelihood_x4p<16>", "bound": "hbm", "unit": "GB/s",
+                   "avg_launch_us": s1_t * 1e6, "algorithmic_bytes_per_launch": s1_bytes,
+                   "achieved": s1_bytes / s1_t / 1e9, "peak": hbm_peak, "frac": s1_bytes / s1_t / 1e9 / hbm_peak,
+                   "peak_source": hbm_src},
+        "stage2": {"kernel": "k_voxel16 (log-odds + bits)", "bound": "l2_gather + hbm_store",
+                   "avg_launch_us": v_t * 1e6,
+                   "gather": {"algorithmic_bytes_per_launch": g_bytes, "lines_per_launch": lines,
+                              "achieved_gbs": g_bytes / v_t / 1e9, "peak_gbs": gather_peak,
+                              "frac": (g_bytes / v_t / 1e9 / gather_peak) if gather_peak else None},
+                   "store": {"bytes_per_launch": st_bytes, "achieved_gbs": st_bytes / v_t / 1e9,
+                             "peak_gbs": hbm_peak, "frac": st_bytes / v_t / 1e9 / hbm_peak},
+                   "frac": bound_t / v_t,
+                   "note": "frac = max(gather bytes / gather probe, store bytes / HBM) / launch time"},
+        "kernel_share": {"stage1": l_ms / max(l_ms + v_ms, 1e-12), "stage2": v_ms / max(l_ms + v_ms, 1e-12)},
+    }
+    del rec, L, Bits
+    return out
+
+
+def variant_leg(args, config, dev, stream, flush, world, nframes=64, pool=16, channels=3, sampling=0,
+                motion=False, note=""):
+    """A secondary configuration through the same API, bits only: frames/s over
+    `nframes`-frame calls cycling `pool` distinct frame sets (host rendering of
+    large frames is slow), L2 flushed between calls."""
+    import torch
+    from paper_1311_6811_b200 import from_scene
+    from synth.scene import CONFIGS, make_frames, make_scene
+    s = make_scene(config, channels=channels)
+    distinct = [torch.from_numpy(make_frames(s, f * 19 if motion else f, motion=motion)).to(dev)
+                for f in range(pool)]
+    rec = from_scene(s, device=dev.index, sampling=sampling)
+    _, Bits = rec.alloc_outputs(nframes, logodds=False)
+    lists = [rec.frame_pointers([distinct[(k * nframes + f) % pool] for f in range(nframes)], nframes)
+             for k in range(4)]
+
+    def step(k):
+        rec.reconstruct_batch(lists[k % 4], nframes, bits=Bits, stream=stream)
+
+    for k in range(2):
+        step(k)
+    torch.cuda.synchronize(dev)
+    ms = timed_calls(step, max(3, min(args.steps, 10)), stream, flush)
+    total = max_over_ranks(sum(ms), world, dev)
+    fps = world * nframes * len(ms) / (total / 1e3)
+    out = {"config": f"{config}: {CONFIGS[config]['desc']}" + (f"; {note}" if note else ""),
+           "frames_per_call": nframes, "distinct_frame_sets": pool, "frames_per_s": fps,
+           "ms_per_frame": 1e3 / fps * world, "voxel_camera_projections_per_s": fps * s.grid.nvox * s.ncam,
+           "call_ms": step_stats(ms), "coarse_passes": rec.coarse_status()[0],
+           "launches_per_call": rec.last_launch_count}
+    del rec, Bits, distinct, lists
+    torch.cuda.empty_cache()
+    return out, s
+
+
+def c1_graph_leg(dev):
+    """C1 (32^3 x 4 cameras at 64x48, BASELINE.json configs[0]): launch-bound, so
+    the call is captured once in a CUDA graph and replayed; device time per
+    replay.  One frame per call (the latency view) and 64 frames per call
+    (one coarse pass)."""
+    import torch
+    from paper_1311_6811_b200 import from_scene
+    from synth.scene import make_frames, make_scene
+    s = make_scene("C1")
+    fr = torch.from_numpy(np.stack([make_frames(s, f) for f in range(64)])).to(dev)
+    out = {"config": "C1: 32^3 grid, 4 cameras at 64x48 (launch-bound; CUDA-graph replays)"}
+    for n in (1, 64):
+        rec = from_scene(s, device=dev.index)
+        _, Bits = rec.alloc_outputs(n, logodds=False)
+        us = device_us(lambda st: rec.reconstruct_batch(fr[:n], n, bits=Bits, stream=st), dev, reps=50)
+        out[f"frames_per_call_{n}"] = {"us_per_call": us, "frames_per_s": n / (us * 1e-6),
+                                       "launches_per_call": rec.last_launch_count}
+    return out
+
+
+def c5_oracle_sample(scene, frame, nthreads):
+    """The oracle on a voxel sample of C5 (C5 is reported as
+    voxel-cam/s on the parity sample, extrapolated to s/frame): 2^14 random voxels,
+    single-threaded and all-core."""
+    import oracle
+    rng = np.random.default_rng(5)
+    vox = np.unique(rng.integers(0, scene.grid.nvox, 1 << 14))
+    res = {}
+    for name, th in (("single_thread", 1), ("all_cores", nthreads)):
+        t0 = time.perf_counter()
+        oracle.fuse_sample(scene.P, scene.widths, scene.heights, scene.grid, frame, scene.mu, scene.sigma,
+                           vox, nthreads=th)
+        el = time.perf_counter() - t0
+        vc = vox.size * scene.ncam / el
+        res[name] = {"threads": th, "voxel_cam_per_s": vc,
+                     "extrapolated_s_per_frame": scene.grid.nvox * scene.ncam / vc}
+    res["sample"] = f"{vox.size} random voxels of one C5 frame (oracle_fuse_sample: Eq 1-9 per voxel-camera)"
+    return res
 
 
 def zslab_bench(args, scene, frames_dev, rank, world, local, dev, stream, variants=None):
@@ -381,14 +592,28 @@ def run_ours(args):
     nvox, ncam = scene.grid.nvox, scene.ncam
     per_cam = frames[0, 0].nbytes
 
-    def step(k):
+    # the ABI's frame-pointer tables, built once: the timed region holds no
+    # Python-side pointer arithmetic
+    tables = {}
+    gathered = []
+
+    def table(k):
         i0 = (k * B) % pool
-        idx = [(i0 + b) % pool for b in range(B)]
-        if idx == list(range(idx[0], idx[0] + B)):
-            fr = frames_dev[idx[0]: idx[0] + B]
-        else:
-            fr = frames_dev[idx]
-        rec.reconstruct_batch(fr, B, logodds=None, bits=Bits, stream=stream)
+        if i0 not in tables:
+            idx = [(i0 + b) % pool for b in range(B)]
+            if idx == list(range(idx[0], idx[0] + B)):
+                fr = frames_dev[idx[0]: idx[0] + B]
+            else:
+                fr = frames_dev[idx].contiguous()
+                gathered.append(fr)
+            tables[i0] = rec.frame_pointers(fr, B)
+        return tables[i0]
+
+    for k in range(args.warmup + args.steps + 2):
+        table(k)
+
+    def step(k):
+        rec.reconstruct_batch(table(k), B, logodds=None, bits=Bits, stream=stream)
 
     for k in range(args.warmup):
         step(k)
@@ -459,11 +684,18 @@ def run_ours(args):
     # k_voxel16's access pattern measured live: lane pairs on two-sector lines of a
     # 64 MB L2-resident table, non-allocating 256-bit loads (psfs_probe_gather_bandwidth)
     wide = coarse and args.coarse_frames > 32  # k_voxel_c8w: 64-byte records, lane pairs
-    if coarse:  # one (narrow) or two (wide) 32-byte sectors per line, 2 blocks/SM, 31 / 62 MB codes
-        gather_peak = (probe_gather_bandwidth((64 if wide else 32) << 20, 2 if wide else 1, 2) / 1e9
-                       if not args.profile else None)
-    else:
-        gather_peak = probe_gather_bandwidth(64 << 20, 2, 3) / 1e9 if not args.profile else None
+    # the probe of the kernel's access pattern at MAXIMUM residency (8 blocks x 256
+    # threads per SM requested; the probe's own register use decides how many are
+    # resident): the pattern's rate, not the kernel's occupancy
+    gather_probe = {}
+    if not args.profile:
+        for bps in (2, 3, 4, 8):
+            gather_probe[bps] = probe_gather_bandwidth((64 if (wide or not coarse) else 32) << 20,
+                                                       2 if (wide or not coarse) else 1, bps) / 1e9
+    gather_peak = max(gather_probe.values()) if gather_probe else None
+    gather_peak_16 = None
+    if not args.profile:  # k_voxel16's pattern (full-output leg): lane pairs on 2-sector lines
+        gather_peak_16 = max(probe_gather_bandwidth(64 << 20, 2, bps) / 1e9 for bps in (3, 8))
     traffic = {}
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -520,22 +752,24 @@ def run_ours(args):
                                        "peak_source": kv["peak_source"]}
         kv.update({"bound": "l2_gather", "peak": gather_peak,
                    "fixups_per_step": fixups / max(args.steps, 1),
-                   "peak_source": ("measured live: psfs_probe_gather_bandwidth(64 MB, 2 sectors/line, "
-                                   "2 blocks/SM) -- lane pairs read both 32-byte sectors of random "
-                                   "128-byte lines of an L2-resident table (k_voxel_c8w's pattern)"
+                   "probe_gbs_by_blocks_per_sm": gather_probe,
+                   "peak_source": ("measured live: psfs_probe_gather_bandwidth(64 MB, 2 sectors/line) -- "
+                                   "lane pairs read both 32-byte sectors of random 128-byte lines of an "
+                                   "L2-resident table (k_voxel_c8w's pattern)"
                                    if wide else
-                                   "measured live: psfs_probe_gather_bandwidth(32 MB, 1 sector/line, "
-                                   "2 blocks/SM) -- every lane reads one 32-byte sector of its own "
-                                   "random 128-byte line of an L2-resident table (k_voxel_c8's pattern)")
-                                  + ", non-allocating 256-bit loads at the kernel's residency; the "
-                                    "timed launch includes k_fixup_c8; DESIGN.md section 8"})
+                                   "measured live: psfs_probe_gather_bandwidth(32 MB, 1 sector/line) -- "
+                                   "every lane reads one 32-byte sector of its own random 128-byte line "
+                                   "of an L2-resident table (k_voxel_c8's pattern)")
+                                  + ", non-allocating 256-bit loads, the best of 2/3/4/8 blocks x 256 "
+                                    "threads per SM (maximum residency, not the kernel's 2); the timed "
+                                    "launch includes k_fixup_c8; DESIGN.md section 8"})
     elif F == 16 and gather_peak:
         # the binding roofline of the 16-frame gather: the same access pattern's
         # measured rate from L2 (the all-hit L1 line rate kept beside it)
         kv = per_kernel["k_voxel"]
         kv["all_hit_l1_line_bound"] = {"peak": kv["peak"], "frac": kv["achieved"] / kv["peak"],
                                        "peak_source": kv["peak_source"]}
-        kv.update({"bound": "l2_gather", "peak": gather_peak,
+        kv.update({"bound": "l2_gather", "peak": gather_peak, "probe_gbs_by_blocks_per_sm": gather_probe,
                    "peak_source": "measured live: psfs_probe_gather_bandwidth(64 MB) -- lane pairs "
                                   "reading both 32-byte sectors of random 128-byte lines of an "
                                   "L2-resident table with k_voxel16's non-allocating 256-bit load "
@@ -765,13 +999,65 @@ def run_ours(args):
                   "note": "NEXT-1 posterior 3x3x3 box filter + threshold (P:111, P:300), "
                           "2 launches (device time, CUDA-graph replay), not part of the headline step"}
 
+    # ---- secondary: the full output (log-odds + bits), the same C2 step
+    full_output = None
+    flush_pair = (flush, flush_rd)
+    if not args.profile and not args.no_secondaries:
+        try:
+            full_output = full_output_leg(args, scene, frames_dev, B, pool, dev, stream, flush_pair, world,
+                                          hbm_peak, gather_peak_16, hbm_src)
+        except Exception as e:
+            full_output = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+
+    # ---- secondary configurations (BASELINE.json configs) and NEXT-3 variants,
+    # bits only, through the same API; reported beside the headline, never as it
+    configs_out = {}
+    c5_scene = None
+    if not args.profile and not args.no_secondaries:
+        legs = [
+            ("C2_grayscale", dict(config="C2", channels=1, note="NEXT-3 grayscale input (U = 256^-1), exact path")),
+            ("C2_bilinear", dict(config="C2", sampling=1, note="NEXT-3 bilinear SLM sampling, 8-frame passes")),
+            ("C3_sequence", dict(config="C3", nframes=300, pool=16, motion=True,
+                                 note="300-frame walking / arm-waving sequence in one call (16 distinct "
+                                      "frame sets of the sequence, every 19th frame, cycled)")),
+        ]
+        if not args.no_c5:
+            legs.append(("C5", dict(config="C5", nframes=64, pool=1,
+                                    note="one 64-frame coarse pass (1 distinct frame set repeated: host "
+                                         "rendering of 32 x 1920x1080 views is slow)")))
+        for name, kw in legs:
+            try:
+                configs_out[name], sc = variant_leg(args, dev=dev, stream=stream, flush=flush_pair,
+                                                    world=world, **kw)
+                if name == "C5":
+                    c5_scene = sc
+            except Exception as e:
+                configs_out[name] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+        try:
+            configs_out["C1"] = c1_graph_leg(dev)
+        except Exception as e:
+            configs_out["C1"] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         nthreads = host_cores()
         v, n, el = cpu_baseline(scene, frames, args.cpu_seconds, nthreads)
+        v1, n1, el1 = cpu_baseline(scene, frames, args.cpu_seconds / 2, 1)
         cpu = {"value": v, "unit": "frames/s", "cores": nthreads, "kind": "oracle",
                "sample": f"{n} full {args.config} frames ({el:.1f} s of work), plain C oracle "
-                         f"(double; OpenMP over z-slices)"}
+                         f"(double; OpenMP over z-slices, {nthreads} threads)",
+               "single_thread": {"value": v1, "unit": "frames/s", "cores": 1,
+                                 "sample": f"{n1} full {args.config} frames ({el1:.1f} s)"},
+               "host": cpu_info(),
+               "gpu_over_oracle": {"all_cores": fps / v, "single_thread": fps / v1,
+                                   "paper_context": "HD 6870 vs one i7-860 core: 399x (P:376), whole pipeline "
+                                                    "incl. APF"}}
+        if c5_scene is not None:
+            try:
+                from synth.scene import make_frames
+                cpu["C5_sample"] = c5_oracle_sample(c5_scene, make_frames(c5_scene, 0), nthreads)
+            except Exception as e:
+                cpu["C5_sample"] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
 
     if rank == 0:
         out = {
@@ -794,10 +1080,9 @@ def run_ours(args):
                        "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the step events)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "carve": carve, "exact_path": exact,
             "single_frame": single, "surface": surface, "color": color, "smooth": smooth,
-            "train": train, "zslab": zslab,
+            "train": train, "zslab": zslab, "full_output": full_output, "configs": configs_out,
             "gpu_launches": launches, "clocks": clocks,
-            "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms),
-                        "max": max(step_ms), "all": [round(x, 4) for x in step_ms]},
+            "step_ms": dict(step_stats(step_ms), all=[round(x, 4) for x in step_ms]),
         }
         print(json.dumps(out), flush=True)
     if world > 1:

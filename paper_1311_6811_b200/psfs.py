@@ -342,8 +342,13 @@ class Reconstructor:
     # -- the hot path ---------------------------------------------------------
     def _frame_ptrs(self, frames, nframes):
         """frames: a uint8 CUDA tensor [nframes, ncam, H, W, 3] (or [ncam, H, W, 3]
-        when nframes == 1), or a nested list [f][c] of [H, W, 3] tensors."""
+        when nframes == 1), a nested list [f][c] of [H, W, 3] tensors, or a
+        pointer table from frame_pointers() (reused as is)."""
         import torch
+        if isinstance(frames, C.Array):
+            if len(frames) < nframes * self.ncam:
+                raise ValueError("pointer table too short")
+            return frames
         ptrs = []
         if isinstance(frames, torch.Tensor):
             t = frames
@@ -364,6 +369,12 @@ class Reconstructor:
                 for c in range(self.ncam):
                     ptrs.append(_dev_ptr(row[c], torch.uint8))
         return _ptr_array(ptrs)
+
+    def frame_pointers(self, frames, nframes: int):
+        """The HOST table of nframes * ncam device frame pointers the ABI takes,
+        built once (e.g. outside a timed loop) and passed back as `frames`; the
+        tensors it points into must stay alive."""
+        return self._frame_ptrs(frames, nframes)
 
     def reconstruct_batch(self, frames, nframes: int, logodds=None, bits=None, stream=None):
         """Enqueue both stages for nframes frame sets on `stream` (default: the
