@@ -223,6 +223,34 @@ int psfs_surface(psfs_handle *h, const uint32_t *bits, uint32_t *surface_bits, i
 int psfs_smooth_threshold(psfs_handle *h, const float *logodds, float *smoothed, uint32_t *bits,
                           void *cuda_stream);
 
+/* NEXT-1 merged with reconstruction, from the exact sums (no float log-odds or
+ * posterior volume in between; "merging this procedure will
+ * significantly improve GPU computing efficiency").  S = sum of the in-view
+ * Q11.20 terms (Eq 3-4), L = S 2^-20 + logit p_V, P = 1/(1 + e^-L), then the
+ * 3x3x3 zero-padded box average and smoothed > tau as psfs_smooth_threshold.
+ *
+ * psfs_reconstruct_sums: both stages of the exact path with the int32 sums as
+ *   the per-voxel output: sums DEVICE, nframes x (this handle's slab, x-fastest)
+ *   int32; bits (nullable) the unsmoothed bitmask as psfs_reconstruct_batch.
+ * psfs_smooth_sums: the smoothing of nframes such slabs.  A z-slab handle
+ *   (psfs_dist world > 1) needs the neighbouring slabs' boundary slices:
+ *   halo_lo = slice k0 - 1 (required when k0 > 0), halo_hi = slice k1 (required
+ *   when k1 < zlen), DEVICE, nframes x xlen*ylen int32 each (the caller moves
+ *   them between ranks: NCCL send/recv in parallel.py); slices past the volume
+ *   are the zero padding.  smoothed (nullable): nframes x slab floats; bits
+ *   (nullable): nframes full-grid word arrays, this slab's words written.
+ * psfs_reconstruct_smoothed: world-1 handles: both in one call per frame group,
+ *   the sums in library scratch (kMaxF frames of the slab).
+ * All asynchronous on cuda_stream.  Errors: PSFS_EINVAL (NULL / missing halo /
+ * world != 1 for psfs_reconstruct_smoothed), PSFS_ESTATE, PSFS_ECOUNT,
+ * PSFS_ENOMEM, PSFS_ECUDA. */
+int psfs_reconstruct_sums(psfs_handle *h, int32_t nframes, const uint8_t *const *frames, int32_t *sums,
+                          uint32_t *bits, void *cuda_stream);
+int psfs_smooth_sums(psfs_handle *h, int32_t nframes, const int32_t *sums, const int32_t *halo_lo,
+                     const int32_t *halo_hi, float *smoothed, uint32_t *bits, void *cuda_stream);
+int psfs_reconstruct_smoothed(psfs_handle *h, int32_t nframes, const uint8_t *const *frames, float *smoothed,
+                              uint32_t *bits, void *cuda_stream);
+
 void psfs_destroy(psfs_handle *h);
 
 const char *psfs_status_string(int status);

@@ -101,6 +101,7 @@ struct VParams {
     int32_t word_rows;         // xlen % 32 == 0: a 32-wide tile row is one bitmask word
     float bl_a, bl_b;          // bilinear sampling (k_voxel_bl): 1 - p_O, 2 p_O - 1
     int32_t lo_pairs;          // k_voxel16: x-adjacent log-odds as 8-byte stores (xlen, lo_stride even, 8-B base)
+    int32_t lo_raw;            // lo_base receives the int32 sums S instead of float log-odds (NEXT-1)
 };
 
 // ---- coarse passes (bits-only calls) -------------------
@@ -256,6 +257,23 @@ struct TrainParams {
 };
 cudaError_t launch_train(const TrainParams &p, cudaStream_t s);
 cudaError_t launch_voxel(const VParams &p, int F, cudaStream_t s, int *nblocks);
+// NEXT-1 from the exact int32 sums (k_box_sums): posterior P = 1 / (1 + e^-L),
+// L = S 2^-20 + logit p_V, 3x3x3 zero-padded box average, occupied := > tau.
+// sums: nf frames of the slab [k0, k1) (frame stride nslab); halo_lo / halo_hi:
+// slices k0 - 1 / k1 of the neighbouring slabs (frame stride xlen * ylen), NULL
+// at the volume's own boundary (zero padding); outputs per frame: smoothed
+// (slab, nullable), bits (full-grid words, slab words written, nullable).
+struct BoxSumsParams {
+    const int32_t *sums;
+    const int32_t *halo_lo, *halo_hi;
+    float *smoothed;
+    uint32_t *bits;
+    int64_t sums_stride, halo_stride, smoothed_stride, bits_stride;
+    int32_t xlen, ylen, zlen, k0, k1, nf;
+    double logit_pv;
+    float tau;
+};
+cudaError_t launch_box_sums(const BoxSumsParams &p, cudaStream_t s);
 int voxel_tiles(int xlen, int ylen, int k0, int k1, int ty, int kz);
 cudaError_t launch_surface(const uint32_t *bits, uint32_t *surf, int64_t *idx, int64_t capacity,
                            int64_t *count, long long *block_scratch, int xlen, int ylen, int zlen,

@@ -140,6 +140,29 @@ cudaError_t launch_s1x(const S1Params &p_in, int F, int nch, bool slm, int max_p
     return cudaErrorInvalidValue;
 }
 
+// One pixel's F-frame SLM record (F * 4 bytes, F * 4-byte aligned) as vector loads.
+template <int F>
+__device__ __forceinline__ void load_rec(const float *src, float (&v)[F])
+{
+    if constexpr (F == 8) {
+        uint32_t w[8];
+        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+                       "=r"(w[7])
+                     : "l"(src));
+#pragma unroll
+        for (int f = 0; f < 8; ++f) v[f] = __uint_as_float(w[f]);
+    } else if constexpr (F == 4) {
+        const float4 a = __ldg(reinterpret_cast<const float4 *>(src));
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    } else if constexpr (F == 2) {
+        const float2 a = __ldg(reinterpret_cast<const float2 *>(src));
+        v[0] = a.x; v[1] = a.y;
+    } else {
+        v[0] = __ldg(src);
+    }
+}
+
 // Stage 2 with bilinear SLM sampling.  A warp is 32 consecutive voxels of the
 // slab (x-fastest), i.e. one bitmask word: slabs start on word boundaries
 // (psfs_create), so lane 0 stores the ballot word.  Per camera: the pinned
@@ -189,13 +212,10 @@ __global__ void __launch_bounds__(256) k_voxel_bl(const __grid_constant__ VParam
             const int64_t ra = (int64_t)p.cam[c].toff + (int64_t)ya * p.cam[c].Wp;
             const int64_t rb = (int64_t)p.cam[c].toff + (int64_t)yb * p.cam[c].Wp;
             float s00[F], s10[F], s01[F], s11[F];
-#pragma unroll
-            for (int f = 0; f < F; ++f) {
-                s00[f] = __ldg(T + (ra + xa) * F + f);
-                s10[f] = __ldg(T + (ra + xb) * F + f);
-                s01[f] = __ldg(T + (rb + xa) * F + f);
-                s11[f] = __ldg(T + (rb + xb) * F + f);
-            }
+            load_rec<F>(T + (ra + xa) * F, s00);
+            load_rec<F>(T + (ra + xb) * F, s10);
+            load_rec<F>(T + (rb + xa) * F, s01);
+            load_rec<F>(T + (rb + xb) * F, s11);
             // weight form (1 - fx) a + fx b: every product and sum is of non-negative
             // values, so the sample keeps a few ulps of relative precision (the lerp
             // a + fx (b - a) loses it where SLM jumps from ~1 to ~1e-4 and the sample
@@ -215,7 +235,7 @@ __global__ void __launch_bounds__(256) k_voxel_bl(const __grid_constant__ VParam
         for (int f = 0; f < F; ++f) {
             const unsigned m = __ballot_sync(0xffffffffu, valid && S[f] > p.Tq);
             if (p.lo_base && valid)
-                p.lo_base[f * p.lo_stride + o] = logodds_of(S[f], p.logit_pv);
+                p.lo_base[f * p.lo_stride + o] = p.lo_raw ? __int_as_float(S[f]) : logodds_of(S[f], p.logit_pv);
             if (lane == 0) {
                 if (p.npeer == 0) {
                     if (p.bits_base) p.bits_base[f * p.bits_stride + word] = m;

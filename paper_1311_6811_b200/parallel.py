@@ -18,6 +18,13 @@ One process per GPU (torchrun), torch.distributed for the plumbing:
   - or by one in-place all-gather of the per-slab words (NCCL over NVLink on
     GPUs; gloo in the CPU tests).
   Log-odds stay sharded.
+* NEXT-1 on z-slabs (reconstruct_smoothed): the 3x3x3 box filter of the
+  posterior needs one slice of each neighbouring slab; every rank computes
+  its slab's exact int32 sums (psfs_reconstruct_sums), sends its first slice
+  to rank - 1 and its last to rank + 1 and receives their boundary slices
+  (exchange_halos: point-to-point send/recv, NCCL on GPUs, gloo on CPU
+  tensors), then smooths and thresholds its slab (psfs_smooth_sums); the
+  smoothed bitmask is all-gathered like the plain one.
 
 The slab rule here is the same pure function the library applies
 (k0 = zlen*rank//world); tests check both agree.
@@ -72,6 +79,34 @@ def allgather_bits(bits, xlen, ylen, zlen, world, rank, group=None):
             dist.all_gather(parts, mine.clone(), group=group)
             row.copy_(torch.cat(parts))
     return bits
+
+
+def exchange_halos(sums, plane: int, world: int, rank: int, group=None):
+    """One-slice halo exchange between neighbouring z-slabs (NEXT-1 on slabs):
+    sums is this rank's [nframes, nslab] int32 tensor; rank r sends slice k0
+    (its first plane) to r - 1 and slice k1 - 1 (its last) to r + 1, and
+    receives slice k0 - 1 from r - 1 (halo_lo) and slice k1 from r + 1
+    (halo_hi).  Returns (halo_lo, halo_hi), None at the volume's boundary.
+    Non-blocking isend/irecv pairs (NCCL for CUDA tensors, gloo for CPU)."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return None, None
+    b = sums if sums.dim() == 2 else sums.unsqueeze(0)
+    first = b[:, :plane].contiguous()
+    last = b[:, b.shape[1] - plane:].contiguous()
+    lo = torch.empty_like(first) if rank > 0 else None
+    hi = torch.empty_like(last) if rank < world - 1 else None
+    reqs = []
+    if rank > 0:
+        reqs.append(dist.isend(first, rank - 1, group=group))
+        reqs.append(dist.irecv(lo, rank - 1, group=group))
+    if rank < world - 1:
+        reqs.append(dist.isend(last, rank + 1, group=group))
+        reqs.append(dist.irecv(hi, rank + 1, group=group))
+    for r in reqs:
+        r.wait()
+    return lo, hi
 
 
 def env_rank_world():
@@ -130,6 +165,39 @@ class ZSlabReconstructor:
             if not all(oks):
                 raise RuntimeError("psfs_peer_open failed on rank(s) "
                                    f"{[r for r, x in enumerate(oks) if not x]}")
+
+    def reconstruct_smoothed(self, frames, nframes, smoothed=None, bits=None, stream=None, gather=True):
+        """NEXT-1 on the z-slab partition: sums of this slab, halo exchange with
+        the neighbours, smoothing + threshold of the slab, and (gather) the
+        smoothed bitmask all-gathered so every rank holds the full grid.
+        smoothed: float32 [nframes, nslab] (nullable); bits: int32 [nframes,
+        nwords].  Returns bits."""
+        import torch
+        import torch.distributed as dist
+        g = self.grid
+        plane = g.xlen * g.ylen
+        dev = torch.device("cuda", self.rec.device)
+        sums = torch.empty((nframes, self.rec.nslab), dtype=torch.int32, device=dev)
+        self.rec.reconstruct_sums(frames, nframes, sums, stream=stream)
+        lo = hi = None
+        if self.world > 1:
+            torch.cuda.synchronize(dev)
+            cpu = dist.get_backend(self.group) != "nccl"  # gloo moves CPU tensors only
+            lo, hi = exchange_halos(sums.cpu() if cpu else sums, plane, self.world, self.rank, self.group)
+            if cpu:
+                lo = lo.to(dev) if lo is not None else None
+                hi = hi.to(dev) if hi is not None else None
+        self.rec.smooth_sums(nframes, sums, lo, hi, smoothed=smoothed, bits=bits, stream=stream)
+        if gather and bits is not None and self.world > 1:
+            torch.cuda.synchronize(dev)
+            cpu = dist.get_backend(self.group) != "nccl"
+            if cpu:
+                b = bits.cpu()
+                allgather_bits(b, g.xlen, g.ylen, g.zlen, self.world, self.rank, self.group)
+                bits.copy_(b.to(dev))
+            else:
+                allgather_bits(bits, g.xlen, g.ylen, g.zlen, self.world, self.rank, self.group)
+        return bits
 
     def reconstruct_batch(self, frames, nframes, logodds=None, bits=None, stream=None,
                           gather=True):

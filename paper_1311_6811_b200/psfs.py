@@ -41,7 +41,7 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_peer_open", "psfs_reconstruct_peer", "psfs_peer_status", "psfs_color",
            "psfs_train_background", "psfs_probe_gather_bandwidth", "psfs_set_coarse",
            "psfs_coarse_plan", "psfs_coarse_status", "psfs_debug_codes", "psfs_set_host_upload",
-           "psfs_set_input"]
+           "psfs_set_input", "psfs_reconstruct_sums", "psfs_smooth_sums", "psfs_reconstruct_smoothed"]
 SAMPLE_NEAREST = 0
 SAMPLE_BILINEAR = 1
 MAX_COARSE = 64
@@ -124,6 +124,9 @@ def lib():
         L.psfs_debug_codes.argtypes = [vp, vp, vp, vp]
         L.psfs_set_host_upload.argtypes = [vp, i32]
         L.psfs_set_input.argtypes = [vp, i32, i32]
+        L.psfs_reconstruct_sums.argtypes = [vp, i32, vp, vp, vp, vp]
+        L.psfs_smooth_sums.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp]
+        L.psfs_reconstruct_smoothed.argtypes = [vp, i32, vp, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -495,6 +498,39 @@ class Reconstructor:
                                                 _dev_ptr(smoothed, torch.float32),
                                                 _dev_ptr(bits, torch.int32), s),
                     "psfs_smooth_threshold")
+        return smoothed, bits
+
+    def reconstruct_sums(self, frames, nframes: int, sums, bits=None, stream=None):
+        """NEXT-1 step 1: both stages with the exact int32 sums S (int32 CUDA tensor
+        [nframes, nslab]) as the per-voxel output; optional unsmoothed bits."""
+        import torch
+        fp = self._frame_ptrs(frames, nframes)
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        if sums.numel() < nframes * self.nslab:
+            raise ValueError("sums too small")
+        self._check(lib().psfs_reconstruct_sums(self._h, int(nframes), fp, _dev_ptr(sums, torch.int32),
+                                                _dev_ptr(bits, torch.int32), s), "psfs_reconstruct_sums")
+
+    def smooth_sums(self, nframes: int, sums, halo_lo=None, halo_hi=None, smoothed=None, bits=None,
+                    stream=None):
+        """NEXT-1 step 2: posterior 3x3x3 box average > tau from the sums; z-slab
+        handles pass the neighbours' boundary slices (int32 [nframes, xlen*ylen])."""
+        import torch
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._check(lib().psfs_smooth_sums(self._h, int(nframes), _dev_ptr(sums, torch.int32),
+                                           _dev_ptr(halo_lo, torch.int32), _dev_ptr(halo_hi, torch.int32),
+                                           _dev_ptr(smoothed, torch.float32), _dev_ptr(bits, torch.int32), s),
+                    "psfs_smooth_sums")
+        return smoothed, bits
+
+    def reconstruct_smoothed(self, frames, nframes: int, smoothed=None, bits=None, stream=None):
+        """NEXT-1 merged with reconstruction (world-1 handles): smoothed posterior
+        (float32 [nframes, nvox], nullable) and its threshold bits."""
+        import torch
+        fp = self._frame_ptrs(frames, nframes)
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._check(lib().psfs_reconstruct_smoothed(self._h, int(nframes), fp, _dev_ptr(smoothed, torch.float32),
+                                                    _dev_ptr(bits, torch.int32), s), "psfs_reconstruct_smoothed")
         return smoothed, bits
 
     # -- introspection ----------------------------------------------------------

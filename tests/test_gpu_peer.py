@@ -20,7 +20,7 @@ import torch.multiprocessing as mp
 
 import oracle
 from synth.scene import Grid, make_frames, make_scene
-from tests.helpers import assert_parity, gpu_run
+from tests.helpers import assert_parity, gpu_run, unpack_bits
 
 NTHREADS = max(1, len(os.sched_getaffinity(0)))
 
@@ -52,9 +52,16 @@ def _worker(rank, world, port, kind, nframes, mode, q):
         from paper_1311_6811_b200.parallel import ZSlabReconstructor
         torch.cuda.set_device(0)
         s = _scene(kind)
-        z = ZSlabReconstructor(s, rank=rank, world=world, device=0, peer=(mode != "allgather"),
+        z = ZSlabReconstructor(s, rank=rank, world=world, device=0, peer=(mode not in ("allgather", "smooth")),
                                max_frames=nframes)
         fr = torch.from_numpy(np.stack([make_frames(s, f) for f in range(nframes)])).cuda()
+        if mode == "smooth":  # NEXT-1 on slabs: sums, halo exchange (gloo), smoothing, all-gather
+            bits = torch.zeros((nframes, s.grid.nwords), dtype=torch.int32, device="cuda")
+            sm = torch.empty((nframes, z.rec.nslab), dtype=torch.float32, device="cuda")
+            z.reconstruct_smoothed(fr, nframes, smoothed=sm, bits=bits)
+            torch.cuda.synchronize()
+            q.put((rank, (bits.cpu().numpy().copy(), sm.cpu().numpy().copy(), z.rec.k0, z.rec.k1)))
+            return
         if mode == "allgather":
             from paper_1311_6811_b200.parallel import allgather_bits
             out = []
@@ -182,3 +189,21 @@ def test_bench_zslab_section():
         assert p.exitcode == 0
     for r in range(2):
         assert res[r]["fused_peer"]["frames_per_s"] > 0
+
+
+@pytest.mark.parametrize("world,nframes", [(2, 2), (4, 3)])
+def test_zslab_smoothing_against_oracle(world, nframes):
+    """NEXT-1 across ranks: each rank's smoothed slab and the all-gathered
+    smoothed bitmask against the oracle's box filter of the full posterior."""
+    res = _run(world, "C1", nframes, mode="smooth")
+    s = _scene("C1")
+    g = s.grid
+    plane = g.xlen * g.ylen
+    for f in range(nframes):
+        orc = oracle.scene_reconstruct(s, make_frames(s, f), nthreads=NTHREADS)
+        sm_o, bits_o = oracle.smooth_threshold(orc["post"], g, 0.5)
+        for r in range(world):
+            bits, sm, k0, k1 = res[r]
+            assert np.abs(sm[f].astype(np.float64) - sm_o[plane * k0: plane * k1]).max() <= 1e-5
+            mism = unpack_bits(bits[f].view(np.uint32), g.nvox) != unpack_bits(bits_o, g.nvox)
+            assert not (mism & ~(np.abs(sm_o - 0.5) < 1e-4)).any()

@@ -126,3 +126,45 @@ def test_exchange_handles_rank_order(world):
     want = [bytes([r]) * 64 for r in range(world)]
     for r in range(world):
         assert results[r] == want
+
+
+def _halo_worker(rank, world, port, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plane, slices, nf = 6, 3, 2
+        # rank r's slab: value = 1000 * frame + global slice index * 10 + x
+        k0 = rank * slices
+        sums = torch.tensor([[1000 * f + (k0 + k) * 10 + x for k in range(slices) for x in range(plane)]
+                             for f in range(nf)], dtype=torch.int32)
+        lo, hi = parallel.exchange_halos(sums, plane, world, rank)
+        result_q.put((rank, (None if lo is None else lo.numpy(), None if hi is None else hi.numpy())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_exchange_halos_neighbour_slices(world):
+    """NEXT-1 on z-slabs: rank r receives slice k0 - 1 (the last slice of rank
+    r - 1) and slice k1 (the first of rank r + 1), none at the volume's ends."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    plane, slices, nf = 6, 3, 2
+    for r in range(world):
+        lo, hi = res[r]
+        k0, k1 = r * slices, (r + 1) * slices
+        want = lambda k: np.array([[1000 * f + k * 10 + x for x in range(plane)] for f in range(nf)])
+        assert (lo is None) == (r == 0) and (hi is None) == (r == world - 1)
+        if lo is not None:
+            assert np.array_equal(lo, want(k0 - 1))
+        if hi is not None:
+            assert np.array_equal(hi, want(k1))
