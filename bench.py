@@ -1009,6 +1009,28 @@ def run_ours(args):
         except Exception as e:
             full_output = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
 
+    # ---- secondary: NEXT-1 merged with reconstruction (exact sums -> k_box_sums),
+    # the same 64 C2 frame sets per call, smoothed bitmask out
+    smooth_merged = None
+    if not args.profile and not args.no_secondaries:
+        try:
+            rs = from_scene(scene, device=local)
+            _, Bs = rs.alloc_outputs(B, logodds=False)
+            tab = rs.frame_pointers(frames_dev[:B], B)
+            rs.reconstruct_smoothed(tab, B, bits=Bs, stream=stream)
+            torch.cuda.synchronize(dev)
+            ms = timed_calls(lambda k: rs.reconstruct_smoothed(tab, B, bits=Bs, stream=stream),
+                             max(3, min(args.steps, 10)), stream, flush_pair)
+            tot = max_over_ranks(sum(ms), world, dev)
+            smooth_merged = {"frames_per_s": world * B * len(ms) / (tot / 1e3), "call_ms": step_stats(ms),
+                             "launches_per_call": rs.last_launch_count,
+                             "note": "NEXT-1 merged (P:269-271): psfs_reconstruct_smoothed, exact int32 sums "
+                                     "(16-frame passes) then k_box_sums (posterior on the fly, 3x3x3 box, "
+                                     "threshold); no float log-odds / posterior volume; smoothed bitmask out"}
+            del rs, Bs
+        except Exception as e:
+            smooth_merged = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+
     # ---- secondary configurations (BASELINE.json configs) and NEXT-3 variants,
     # bits only, through the same API; reported beside the headline, never as it
     configs_out = {}
@@ -1080,7 +1102,8 @@ def run_ours(args):
                        "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the step events)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "carve": carve, "exact_path": exact,
             "single_frame": single, "surface": surface, "color": color, "smooth": smooth,
-            "train": train, "zslab": zslab, "full_output": full_output, "configs": configs_out,
+            "train": train, "zslab": zslab, "full_output": full_output, "smooth_merged": smooth_merged,
+            "configs": configs_out,
             "gpu_launches": launches, "clocks": clocks,
             "step_ms": dict(step_stats(step_ms), all=[round(x, 4) for x in step_ms]),
         }
