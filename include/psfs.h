@@ -67,6 +67,7 @@ enum {
 #define PSFS_MAX_PEERS 8    /* ranks of one fused peer exchange (one node) */
 #define PSFS_MAX_TRAIN_FRAMES 512 /* frames of one psfs_train_background call */
 #define PSFS_IPC_HANDLE_BYTES 64 /* size of one exported peer buffer handle */
+#define PSFS_MC_HANDLE_BYTES 64  /* size of the exported multicast object handle (fabric handle) */
 #define PSFS_SAMPLE_NEAREST 0  /* the pixel nearest the projected voxel centre (R#10) */
 #define PSFS_SAMPLE_BILINEAR 1 /* bilinear SLM sample, clamped at the borders (R#26) */
 
@@ -424,6 +425,31 @@ int psfs_peer_open(psfs_handle *h, const void *handles);
 int psfs_reconstruct_peer(psfs_handle *h, int32_t nframes, const uint8_t *const *frames,
                           float *logodds, void *cuda_stream);
 int psfs_peer_status(psfs_handle *h, void *cuda_stream);
+
+/* NVLS multicast bitmask buffer for the fused exchange (SURVEY.md 8(e) stretch:
+ * "k_voxel stores ballot words through an NVLS multicast address"): with it,
+ * psfs_reconstruct_peer sends every bitmask word once, as a multimem store the
+ * NVSwitch replicates into every rank's copy (per-rank NVLink egress 1x the
+ * slab instead of (world - 1)x), and the coarse fix-up patches bits with
+ * multimem reductions (no peer atomics needed).  The IPC peer buffers of
+ * psfs_peer_alloc / psfs_peer_open stay in use for the device barriers.  Setup,
+ * every rank in order, host barriers between the steps:
+ *   psfs_mc_create(h, nframes, handle_out): sizes the buffer (nframes bitmasks);
+ *     rank 0 creates the multicast object (world devices) and writes its fabric
+ *     handle (PSFS_MC_HANDLE_BYTES, HOST) for the others; other ranks write zeros;
+ *   psfs_mc_attach(h, handle): ranks != 0 import rank 0's handle; every rank
+ *     adds its device;  -- barrier: every device added --
+ *   psfs_mc_bind(h, &bits): allocates this device's replica, binds it, maps the
+ *     multicast and the local views; *bits = the local view (DEVICE, nframes
+ *     full-grid bitmasks, valid after psfs_reconstruct_peer's exit barrier).
+ *   -- barrier: every replica bound --
+ * psfs_mc_release drops it (psfs_destroy does too).  Errors: PSFS_ESTATE when
+ * the driver, the device or the fabric has no multicast support (the caller
+ * keeps the N-store peer exchange), PSFS_EINVAL, PSFS_ECUDA. */
+int psfs_mc_create(psfs_handle *h, int32_t nframes, void *handle_out);
+int psfs_mc_attach(psfs_handle *h, const void *handle);
+int psfs_mc_bind(psfs_handle *h, uint32_t **bits_out);
+int psfs_mc_release(psfs_handle *h);
 
 /* Per-kernel device timing (bench instrumentation): when enabled, every
  * stage-1 and stage-2 launch is bracketed by CUDA events on the launching

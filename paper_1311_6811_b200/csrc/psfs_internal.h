@@ -102,6 +102,7 @@ struct VParams {
     float bl_a, bl_b;          // bilinear sampling (k_voxel_bl): 1 - p_O, 2 p_O - 1
     int32_t lo_pairs;          // k_voxel16: x-adjacent log-odds as 8-byte stores (xlen, lo_stride even, 8-B base)
     int32_t lo_raw;            // lo_base receives the int32 sums S instead of float log-odds (NEXT-1)
+    int32_t peer_mc;           // peer[0] is a multicast (NVLS) mapping: multimem stores / reductions
 };
 
 // ---- coarse passes (bits-only calls) -------------------
@@ -164,6 +165,7 @@ struct VCParams {
     unsigned long long *fix_list;
     unsigned long long *fix_head;  // [0] entries, [1] k_fixup_c8 blocks done (reset by its last block)
     uint64_t fix_cap;
+    int32_t peer_mc;          // peer[0] is a multicast (NVLS) mapping: multimem stores / reductions
 };
 
 cudaError_t launch_likelihood_coarse(const S1CParams &p, int max_roi_px, cudaStream_t s);
@@ -274,6 +276,10 @@ struct BoxSumsParams {
     float tau;
 };
 cudaError_t launch_box_sums(const BoxSumsParams &p, cudaStream_t s);
+// Fill words [w0, w1) of nf frames (frame stride fstride) through a multicast
+// (NVLS) mapping: every replica receives the value (multimem.st).
+cudaError_t launch_mc_fill(uint32_t *mc, int64_t fstride, int64_t w0, int64_t w1, int nf, uint32_t value,
+                           cudaStream_t s);
 int voxel_tiles(int xlen, int ylen, int k0, int k1, int ty, int kz);
 cudaError_t launch_surface(const uint32_t *bits, uint32_t *surf, int64_t *idx, int64_t capacity,
                            int64_t *count, long long *block_scratch, int xlen, int ylen, int zlen,

@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(256) k_voxel_bl(const __grid_constant__ VParam
                 if (p.npeer == 0) {
                     if (p.bits_base) p.bits_base[f * p.bits_stride + word] = m;
                 } else {
-                    for (int r = 0; r < p.npeer; ++r) p.peer[r][f * p.peer_fstride + word] = m;
+                    for (int r = 0; r < p.npeer; ++r) peer_store_word(&p.peer[r][f * p.peer_fstride + word], m, p.peer_mc);
                 }
             }
         }

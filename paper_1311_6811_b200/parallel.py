@@ -131,7 +131,7 @@ class ZSlabReconstructor:
     or an NCCL all-gather of the slab words (peer=False)."""
 
     def __init__(self, scene, params=None, rank=None, world=None, device=None, group=None,
-                 peer=False, max_frames=16):
+                 peer=False, max_frames=16, multicast=False):
         from .psfs import from_scene
         r, w, local = env_rank_world()
         self.rank = r if rank is None else rank
@@ -144,6 +144,7 @@ class ZSlabReconstructor:
                               rank=self.rank, world=self.world)
         self.peer = peer
         self.bits = None
+        self.multicast = False
         if peer:
             # host collectives at setup only: every rank maps every other rank's
             # buffer; a failure on any rank makes every rank raise (no rank is
@@ -165,6 +166,42 @@ class ZSlabReconstructor:
             if not all(oks):
                 raise RuntimeError("psfs_peer_open failed on rank(s) "
                                    f"{[r for r, x in enumerate(oks) if not x]}")
+            self.multicast = bool(multicast) and self._setup_multicast(max_frames)
+
+    def _setup_multicast(self, max_frames):
+        """NVLS multicast buffer for the bitmask (include/psfs.h psfs_mc_*): rank 0
+        creates, every rank attaches its device, then binds its replica, with a
+        host agreement after each step; any failure on any rank releases it
+        everywhere and the exchange keeps the per-rank peer stores."""
+        def agree(ok):
+            return all(exchange_handles(b"1" if ok else b"", self.world, self.group))
+
+        try:
+            h = self.rec.mc_create(max_frames)
+            ok = True
+        except Exception:
+            h, ok = b"", False
+        handles = exchange_handles(h, self.world, self.group)
+        if agree(ok):
+            try:
+                self.rec.mc_attach(handles[0])
+                ok = True
+            except Exception:
+                ok = False
+            if agree(ok):  # every device added before any replica is bound
+                try:
+                    bits = self.rec.mc_bind()
+                    ok = True
+                except Exception:
+                    ok = False
+                if agree(ok):
+                    self.bits = bits
+                    return True
+        try:
+            self.rec.mc_release()
+        except Exception:
+            pass
+        return False
 
     def reconstruct_smoothed(self, frames, nframes, smoothed=None, bits=None, stream=None, gather=True):
         """NEXT-1 on the z-slab partition: sums of this slab, halo exchange with

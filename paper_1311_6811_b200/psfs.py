@@ -41,7 +41,9 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_peer_open", "psfs_reconstruct_peer", "psfs_peer_status", "psfs_color",
            "psfs_train_background", "psfs_probe_gather_bandwidth", "psfs_set_coarse",
            "psfs_coarse_plan", "psfs_coarse_status", "psfs_debug_codes", "psfs_set_host_upload",
-           "psfs_set_input", "psfs_reconstruct_sums", "psfs_smooth_sums", "psfs_reconstruct_smoothed"]
+           "psfs_set_input", "psfs_reconstruct_sums", "psfs_smooth_sums", "psfs_reconstruct_smoothed",
+           "psfs_mc_create", "psfs_mc_attach", "psfs_mc_bind", "psfs_mc_release"]
+MC_HANDLE_BYTES = 64
 SAMPLE_NEAREST = 0
 SAMPLE_BILINEAR = 1
 MAX_COARSE = 64
@@ -127,6 +129,10 @@ def lib():
         L.psfs_reconstruct_sums.argtypes = [vp, i32, vp, vp, vp, vp]
         L.psfs_smooth_sums.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp]
         L.psfs_reconstruct_smoothed.argtypes = [vp, i32, vp, vp, vp, vp]
+        L.psfs_mc_create.argtypes = [vp, i32, vp]
+        L.psfs_mc_attach.argtypes = [vp, vp]
+        L.psfs_mc_bind.argtypes = [vp, C.POINTER(vp)]
+        L.psfs_mc_release.argtypes = [vp]
         _lib = L
     return _lib
 
@@ -415,6 +421,39 @@ class Reconstructor:
             bits = torch.as_tensor(_View(), device=torch.device("cuda", self.device))
         self._peer_bits = bits
         return bits, hbuf.raw
+
+    # -- NVLS multicast bitmask buffer (include/psfs.h psfs_mc_*) ----------------
+    def mc_create(self, nframes: int) -> bytes:
+        """Size the multicast buffer; rank 0 creates the object and returns its
+        handle bytes (other ranks: zeros)."""
+        hbuf = C.create_string_buffer(MC_HANDLE_BYTES)
+        self._check(lib().psfs_mc_create(self._h, int(nframes), hbuf), "psfs_mc_create")
+        self._mc_frames = int(nframes)
+        return hbuf.raw
+
+    def mc_attach(self, handle: bytes):
+        buf = C.create_string_buffer(bytes(handle), MC_HANDLE_BYTES)
+        self._check(lib().psfs_mc_attach(self._h, buf), "psfs_mc_attach")
+
+    def mc_bind(self):
+        """Bind this device's replica; returns an int32 CUDA tensor [nframes,
+        nwords] viewing it (the full-grid bitmasks after psfs_reconstruct_peer)."""
+        import torch
+        ptr = C.c_void_p()
+        self._check(lib().psfs_mc_bind(self._h, C.byref(ptr)), "psfs_mc_bind")
+        nwords = self.grid.nwords
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (self._mc_frames, nwords), "typestr": "<i4",
+                                        "data": (int(ptr.value), False), "version": 2, "strides": None}
+        with torch.cuda.device(self.device):
+            bits = torch.as_tensor(_View(), device=torch.device("cuda", self.device))
+        self._mc_bits = bits
+        return bits
+
+    def mc_release(self):
+        self._mc_bits = None
+        self._check(lib().psfs_mc_release(self._h), "psfs_mc_release")
 
     def peer_open(self, handles):
         """handles: list of world IPC handle byte strings in rank order."""

@@ -207,3 +207,30 @@ def test_zslab_smoothing_against_oracle(world, nframes):
             assert np.abs(sm[f].astype(np.float64) - sm_o[plane * k0: plane * k1]).max() <= 1e-5
             mism = unpack_bits(bits[f].view(np.uint32), g.nvox) != unpack_bits(bits_o, g.nvox)
             assert not (mism & ~(np.abs(sm_o - 0.5) < 1e-4)).any()
+
+
+@pytest.mark.parametrize("kind,nframes", [("C1", 3), ("C1", 17), ("ragged", 2)])
+def test_multicast_exchange_single_rank(kind, nframes):
+    """The NVLS multicast variant of the fused exchange (psfs_mc_*), exercised
+    on the one GPU a call gets: a multicast object with one device, bitmask
+    words as multimem stores, ragged rows as multimem OR reductions into
+    cleared words, coarse fix-ups as multimem OR / AND.  The bitmask in the
+    replica equals the plain path's and meets the oracle.  Where the driver /
+    fabric has no multicast, the fallback (peer stores) is what is checked."""
+    from paper_1311_6811_b200.parallel import ZSlabReconstructor
+    s = _scene(kind)
+    frames = [make_frames(s, f) for f in range(nframes)]
+    z = ZSlabReconstructor(s, rank=0, world=1, device=0, peer=True, max_frames=nframes, multicast=True)
+    # where the driver / fabric refuses the multicast object (cuMulticastCreate on
+    # the single-GPU test boxes), setup must fall back cleanly to the peer stores,
+    # and the same checks run on that path
+    print("multicast" if z.multicast else "multicast unavailable: peer-store fallback")
+    fr = torch.from_numpy(np.stack(frames)).cuda()
+    for rep in range(2):
+        bits = z.reconstruct_batch(fr if rep == 0 else fr.flip(0).contiguous(), nframes)
+        z.rec.peer_status()
+        got = bits.cpu().numpy().view(np.uint32).copy()
+        want = frames if rep == 0 else frames[::-1]
+        ref = gpu_run(s, want, fuse=16)["bits"]
+        assert np.array_equal(got, ref)
+        _oracle_bits_check(s, want, got)
