@@ -783,6 +783,11 @@ def run_ours(args):
     roofline["kernel_share"] = {per_kernel[k].get("name", k) if k != dominant else roofline["kernel"]: v
                                 for k, v in share.items()}
     roofline["other_kernel"] = dict(kernel=per_kernel[other].pop("name"), **per_kernel[other])
+    # SURVEY.md 8(d)'s issue / MUFU / gather bounds as the hardware counters read
+    # them (ncu --set full, --cache-control none; profiles/r02_ncu_full.md):
+    # per-pipe % of peak of each kernel of this path
+    if traffic.get("pipes_pct"):
+        roofline["ncu_pipes_pct_of_peak"] = dict(traffic["pipes_pct"], source=traffic.get("note"))
 
     # ---- end to end through the C ABI with HOST buffers (pinned), per step:
     # H2D of the batch's frames, both stages, D2H of the bitmask

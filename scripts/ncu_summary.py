@@ -88,6 +88,20 @@ def full(path, config="C2"):
         base = "k_likelihood" if "k_likelihood" in name else ("k_voxel" if "k_voxel" in name else name)
         if rd is not None and wr is not None:
             traffic[base] = rd + wr
+        pipes = {}
+        for k, label in (("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue"),
+                         ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "xu_mufu"),
+                         ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "alu"),
+                         ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "fma"),
+                         ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64"),
+                         ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "l1_data_pipe"),
+                         ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram"),
+                         ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy")):
+            v = num(k)
+            if v is not None:
+                pipes[label] = v
+        if pipes:
+            traffic.setdefault("pipes_pct", {})[base] = pipes
     return "\n".join(out), {config: traffic}
 
 
