@@ -521,18 +521,25 @@ def zslab_bench(args, scene, frames_dev, rank, world, local, dev, stream, varian
     import torch.distributed as dist
     from paper_1311_6811_b200.parallel import ZSlabReconstructor
     if variants is None:
-        variants = ((("fused_peer", True), ("nccl_allgather", False)) if world > 1
-                    else (("single_gpu", False),))
+        variants = ((("fused_peer", True), ("nccl_allgather", False), ("smoothed_nccl_halo", False))
+                    if world > 1 else (("single_gpu", False), ("smoothed", False)))
     nf = int(frames_dev.shape[0])
     fr = frames_dev.contiguous()
     g = scene.grid
     out = {"frames_per_call": nf, "slices_per_rank": g.zlen // world, "world": world}
     for name, peer in variants:
+        smooth = name.startswith("smoothed")
         z = ZSlabReconstructor(scene, rank=rank, world=world, device=local, peer=peer,
                                max_frames=nf)
         bits = None if peer else torch.zeros((nf, g.nwords), dtype=torch.int32, device=dev)
+        # the smoothed variant materialises the int32 sums of its frames (512 MiB per
+        # C4 frame at N = 1): 16 frames per call
+        nfc = min(nf, 16) if smooth else nf
+        frc = fr[:nfc]
+        call = (lambda: z.reconstruct_smoothed(frc, nfc, bits=bits, stream=stream)) if smooth else \
+            (lambda: z.reconstruct_batch(fr, nf, bits=bits, stream=stream))
         for _ in range(2):
-            z.reconstruct_batch(fr, nf, bits=bits, stream=stream)
+            call()
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
@@ -540,7 +547,7 @@ def zslab_bench(args, scene, frames_dev, rank, world, local, dev, stream, varian
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(reps):
-            z.reconstruct_batch(fr, nf, bits=bits, stream=stream)
+            call()
         e1.record(stream)
         torch.cuda.synchronize(dev)
         if peer:
@@ -548,8 +555,8 @@ def zslab_bench(args, scene, frames_dev, rank, world, local, dev, stream, varian
         t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item()) / reps / nf
-        out[name] = {"ms_per_frame": ms, "frames_per_s": 1e3 / ms,
+        ms = float(t.item()) / reps / nfc
+        out[name] = {"ms_per_frame": ms, "frames_per_s": 1e3 / ms, "frames_per_call": nfc,
                      "voxel_camera_projections_per_s": g.nvox * scene.ncam * 1e3 / ms}
         del z
     return out

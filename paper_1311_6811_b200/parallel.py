@@ -218,15 +218,15 @@ class ZSlabReconstructor:
         self.rec.reconstruct_sums(frames, nframes, sums, stream=stream)
         lo = hi = None
         if self.world > 1:
-            torch.cuda.synchronize(dev)
-            cpu = dist.get_backend(self.group) != "nccl"  # gloo moves CPU tensors only
+            # NCCL: stream-ordered after the sums (torch's current stream); gloo
+            # moves CPU tensors only (the .cpu() copy synchronizes)
+            cpu = dist.get_backend(self.group) != "nccl"
             lo, hi = exchange_halos(sums.cpu() if cpu else sums, plane, self.world, self.rank, self.group)
             if cpu:
                 lo = lo.to(dev) if lo is not None else None
                 hi = hi.to(dev) if hi is not None else None
         self.rec.smooth_sums(nframes, sums, lo, hi, smoothed=smoothed, bits=bits, stream=stream)
         if gather and bits is not None and self.world > 1:
-            torch.cuda.synchronize(dev)
             cpu = dist.get_backend(self.group) != "nccl"
             if cpu:
                 b = bits.cpu()
