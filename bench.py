@@ -52,9 +52,9 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--ty", type=int, default=1)
     ap.add_argument("--kz", type=int, default=4)
-    ap.add_argument("--stage1", type=int, default=0, choices=[0, 1, 2, 3, 4, 5],
+    ap.add_argument("--stage1", type=int, default=6, choices=[0, 1, 2, 3, 4, 5, 6],
                     help="stage-1 kernel: 0 one pixel/thread, 1 TMA ring, 2 pipelined, "
-                         "3 four pixels/thread, 4 warp-row loads (A/B experiments)")
+                         "3 four pixels/thread, 4 warp-row loads, 5 cp.async ring, 6 persistent 4-pixel (default)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-zslab", action="store_true", help="skip the C4 z-slab section")
