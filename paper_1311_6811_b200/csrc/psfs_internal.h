@@ -166,6 +166,16 @@ struct VCParams {
     unsigned long long *fix_head;  // [0] entries, [1] k_fixup_c8 blocks done (reset by its last block)
     uint64_t fix_cap;
     int32_t peer_mc;          // peer[0] is a multicast (NVLS) mapping: multimem stores / reductions
+    // tail-drained fix-up (non-null tile_flag): entries are stored + 1 (0 = not yet
+    // written); a voxel block publishes tile_flag[tile] = pass_id once the tile's
+    // words are flushed and counts itself in fix_head[3] when it has no tiles left;
+    // k_fixup_c8 then needs no grid-wide wait: it claims entries (fix_head[2]) as
+    // the voxel grid's last tiles run, waits only for the entry's own tile, and
+    // zeroes the slots it consumed
+    uint32_t *tile_flag;
+    uint32_t pass_id;
+    int32_t vox_blocks;       // blocks of the voxel launch (producers)
+    int32_t ntx, nty;         // tile grid (the fix-up maps a voxel to its tile)
 };
 
 cudaError_t launch_likelihood_coarse(const S1CParams &p, int max_roi_px, cudaStream_t s);
