@@ -55,6 +55,7 @@ struct S1Params {
     int32_t tf;      // frames per term record (the pass's F: 1..16)
     int32_t halves;  // 2: a 16-frame pass run as two 8-frame halves (path 0/4 only)
     int32_t n4;      // path 6: 4-pixel groups over all cameras (cam[c].pad_[0] = camera c's first)
+    int32_t n2;      // path 6 with 2-pixel threads: 2-pixel groups (cam[c].pad_[1] = camera c's first)
 };
 
 // Stage 2 (voxel) launch description.

@@ -87,7 +87,7 @@ def exchange_halos(sums, plane: int, world: int, rank: int, group=None):
     (its first plane) to r - 1 and slice k1 - 1 (its last) to r + 1, and
     receives slice k0 - 1 from r - 1 (halo_lo) and slice k1 from r + 1
     (halo_hi).  Returns (halo_lo, halo_hi), None at the volume's boundary.
-    Non-blocking isend/irecv pairs (NCCL for CUDA tensors, gloo for CPU)."""
+    One batch of isend/irecv (NCCL for CUDA tensors, gloo for CPU)."""
     import torch
     import torch.distributed as dist
     if world == 1:
@@ -97,15 +97,18 @@ def exchange_halos(sums, plane: int, world: int, rank: int, group=None):
     last = b[:, b.shape[1] - plane:].contiguous()
     lo = torch.empty_like(first) if rank > 0 else None
     hi = torch.empty_like(last) if rank < world - 1 else None
-    reqs = []
+    # one batch (ncclGroupStart/End under NCCL): separate sends posted before the
+    # matching receives would serialise on the pair's stream and deadlock
+    ops = []
     if rank > 0:
-        reqs.append(dist.isend(first, rank - 1, group=group))
-        reqs.append(dist.irecv(lo, rank - 1, group=group))
+        ops.append(dist.P2POp(dist.isend, first, rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, lo, rank - 1, group))
     if rank < world - 1:
-        reqs.append(dist.isend(last, rank + 1, group=group))
-        reqs.append(dist.irecv(hi, rank + 1, group=group))
-    for r in reqs:
-        r.wait()
+        ops.append(dist.P2POp(dist.isend, last, rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, hi, rank + 1, group))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
     return lo, hi
 
 
