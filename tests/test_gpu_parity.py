@@ -350,3 +350,55 @@ def test_full_size_sixteen_frame_pass(name, with_logodds):
         mism = bits != (post > 0.5)
         assert not (mism & ~(np.abs(post - 0.5) < 1e-4)).any()
         assert bits.sum() > 0
+
+
+# ------------------------------------------------------------------ bench launch configurations (round 2 legs)
+
+def test_c3_sequence_300_frames_one_call():
+    """bench.py's C3 leg: the 300-frame walking / arm-waving sequence (16
+    distinct frame sets of it, cycled) in ONE call (coarse passes of <= 64
+    frames); frames 0, 150 and 299 against the oracle on the full 256^3 grid."""
+    from paper_1311_6811_b200 import from_scene
+    s = make_scene("C3")
+    distinct = [make_frames(s, f * 19, motion=True) for f in range(16)]
+    dev = [torch.from_numpy(d).cuda() for d in distinct]
+    rec = from_scene(s)
+    n = 300
+    tab = rec.frame_pointers([dev[f % 16] for f in range(n)], n)
+    _, B = rec.alloc_outputs(n, logodds=False)
+    rec.reconstruct_batch(tab, n, bits=B)
+    torch.cuda.synchronize()
+    assert rec.coarse_status()[0]
+    for f in (0, 150, 299):
+        orc = oracle.scene_reconstruct(s, distinct[f % 16], nthreads=NTHREADS)
+        assert_parity(None, B[f].cpu().numpy().view(np.uint32), orc, s.grid.nvox)
+
+
+def test_c5_coarse_pass_64_frames_sampled():
+    """bench.py's C5 leg: one 64-frame coarse pass of 1024^3 voxels x 32 cameras
+    (the frame-pointer table of 2048 entries), checked on the voxel sample
+    against the oracle for two distinct frame sets, repeats bit-identical."""
+    from paper_1311_6811_b200 import from_scene
+    s = make_scene("C5")
+    two = [make_frames(s, 0), make_frames(s, 1)]
+    dev = [torch.from_numpy(d).cuda() for d in two]
+    rec = from_scene(s)
+    n = 64
+    tab = rec.frame_pointers([dev[f % 2] for f in range(n)], n)
+    _, B = rec.alloc_outputs(n, logodds=False)
+    rec.reconstruct_batch(tab, n, bits=B)
+    torch.cuda.synchronize()
+    assert rec.coarse_status()[0]
+    for f in range(2, n, 7):
+        assert torch.equal(B[f], B[f % 2])
+    rng = np.random.default_rng(23)
+    vox = _sample_voxels(s.grid, rng)
+    vt = torch.from_numpy(vox).cuda()
+    for f in range(2):
+        _, post = oracle.fuse_sample(s.P, s.widths, s.heights, s.grid, two[f], s.mu, s.sigma, vox,
+                                     nthreads=NTHREADS)
+        words = B[f][(vt >> 5)].cpu().numpy().view(np.uint32)
+        bits = ((words >> (vox & 31).astype(np.uint32)) & 1).astype(bool)
+        mism = bits != (post > 0.5)
+        assert not (mism & ~(np.abs(post - 0.5) < 1e-4)).any()
+        assert bits.sum() > 0
