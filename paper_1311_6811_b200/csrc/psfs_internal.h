@@ -177,6 +177,7 @@ struct VCParams {
     uint32_t pass_id;
     int32_t vox_blocks;       // blocks of the voxel launch (producers)
     int32_t ntx, nty;         // tile grid (the fix-up maps a voxel to its tile)
+    int32_t max_blocks_per_sm; // 0: fill the SMs (occupancy); > 0: cap (room for a concurrent stage 1)
 };
 
 cudaError_t launch_likelihood_coarse(const S1CParams &p, int max_roi_px, cudaStream_t s);
