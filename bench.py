@@ -362,8 +362,9 @@ def max_over_ranks(ms, world, dev):
 
 
 def roi_pixels(rec):
-    roi = rec.roi()
-    return int(((roi[:, 1] - roi[:, 0]).astype(np.int64) * (roi[:, 3] - roi[:, 2])).sum())
+    """Stage-1 pixels of one frame set as the library plans them (per-row spans
+    of the region of interest; psfs_roi_pixels)."""
+    return rec.roi_pixels()
 
 
 def full_output_leg(args, scene, frames_dev, B, pool, dev, stream, flush, world, hbm_peak, gather_peak,
@@ -709,8 +710,7 @@ def run_ours(args):
             traffic = json.load(f).get(args.config + ("_coarse" if coarse else ""), {})
     except Exception:
         pass
-    roi = rec.roi()
-    roi_px = int(((roi[:, 1] - roi[:, 0]).astype(np.int64) * (roi[:, 3] - roi[:, 2])).sum())
+    roi_px = roi_pixels(rec)  # stage-1 pixels (per-row spans of the ROI)
     F = args.coarse_frames if coarse else args.fuse
     l_ms, l_n = kt["k_likelihood"]
     v_ms, v_n = kt["k_voxel"]
@@ -820,12 +820,11 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": world * B * args.steps / (e_ms / 1e3), "unit": "frames/s",
-               "h2d_bytes_per_step": int(B * 3 * ((roi[:, 1] - roi[:, 0]).astype(np.int64)
-                                                  * (roi[:, 3] - roi[:, 2])).sum()),
+               "h2d_bytes_per_step": int(B * 3 * roi_px),
                "d2h_bytes_per_step": int(B * scene.grid.nwords * 4),
                "ms_per_step": e_ms / args.steps,
-               "how": "psfs_reconstruct_host: pinned host frames (the region-of-interest rectangle "
-                      "of each image, read over PCIe by the zero-copy upload kernel k_h2d_rows on a "
+               "how": "psfs_reconstruct_host: pinned host frames (the per-row spans of each image's "
+                      "region of interest, read over PCIe by the zero-copy upload kernel k_h2d_rows on a "
                       "copy stream) -> device staging, both stages, bitmask -> pinned host (second "
                       "copy stream), double-buffered"}
 

@@ -271,13 +271,19 @@ int psfs_debug_matrices(const psfs_handle *h, float *out);
 int psfs_debug_terms(psfs_handle *h, const uint8_t *const *frames, int32_t *terms_out,
                      void *cuda_stream);
 
+/* The stage-1 work of one frame set: the pixels of the per-row spans of the
+ * region of interest (the columns each row's slab hull covers, 4-aligned), or
+ * of the rectangles where spans do not apply (psfs_debug_roi).  HOST out.
+ * Errors: PSFS_EINVAL, PSFS_ESTATE (no cameras). */
+int psfs_roi_pixels(const psfs_handle *h, int64_t *pixels);
+
 /* Per-camera stage-1 region of interest the planner computed for this
  * handle's slab: HOST out, ncam*4 int32 (row0, row1, col0, col1), half-open;
  * every pixel a voxel of the slab can project to lies inside it. */
 int psfs_debug_roi(const psfs_handle *h, int32_t *out);
 
 /* Enable/disable the ROI restriction of stage 1 (default on). */
-int psfs_set_roi_enabled(psfs_handle *h, int32_t enabled);
+int psfs_set_roi_enabled(psfs_handle *h, int32_t enabled);  /* 2: rectangles without per-row spans */
 
 /* Stage-1 kernel of the exact path: 0 = one pixel per thread; 1 = TMA
  * bulk-copy ring (needs every W % 16 == 0 and 16-byte aligned frames); 2 =

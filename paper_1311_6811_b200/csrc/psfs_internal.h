@@ -56,6 +56,11 @@ struct S1Params {
     int32_t halves;  // 2: a 16-frame pass run as two 8-frame halves (path 0/4 only)
     int32_t n4;      // path 6: 4-pixel groups over all cameras (cam[c].pad_[0] = camera c's first)
     int32_t n2;      // path 6 with 2-pixel threads: 2-pixel groups (cam[c].pad_[1] = camera c's first)
+    // per-row spans (nullable): row entry i = (camera | row << 8, first column),
+    // span_pre[i] = 4-pixel groups before entry i, span_chunk[k] = the entry of
+    // group 256 k; when set, n4 counts the spans' groups
+    const int32_t *span_info, *span_pre, *span_chunk;
+    int32_t span_rows;
 };
 
 // Stage 2 (voxel) launch description.
@@ -129,6 +134,8 @@ struct S1CParams {
     double lr;           // ln(1 - p_O) - ln p_O
     float s;             // 2^(20 - sh)
     float zoff;          // (-ln p_O - eps) s + bias
+    const int32_t *span_info, *span_pre, *span_chunk;  // per-row spans (as S1Params), nullable
+    int32_t span_rows;
 };
 
 struct VCCam {
@@ -210,6 +217,10 @@ struct H2DParams {
     int32_t task_begin[kMaxCam + 1];      // row tasks of camera c in one frame: [task_begin[c], task_begin[c+1])
     int32_t nf, ncam;
     int32_t bpp;      // bytes per pixel (3 RGB, 1 grayscale)
+    // per-row spans (nullable): one task per (frame, row entry) uploading the
+    // span's columns [cs, cs + 4 groups) instead of the rectangle's row
+    const int32_t *span_info, *span_pre;
+    int32_t span_rows;
     int32_t aligned;  // 16: every image and staging image 16-byte aligned with a whole number of
                       // 16-byte chunks (chunked copy); 4: every row segment 4-byte aligned; 1: bytes
 };

@@ -42,7 +42,7 @@ EXPORTS = ["psfs_default_params", "psfs_create", "psfs_set_cameras", "psfs_set_b
            "psfs_train_background", "psfs_probe_gather_bandwidth", "psfs_set_coarse",
            "psfs_coarse_plan", "psfs_coarse_status", "psfs_debug_codes", "psfs_set_host_upload",
            "psfs_set_input", "psfs_reconstruct_sums", "psfs_smooth_sums", "psfs_reconstruct_smoothed",
-           "psfs_mc_create", "psfs_mc_attach", "psfs_mc_bind", "psfs_mc_release"]
+           "psfs_mc_create", "psfs_mc_attach", "psfs_mc_bind", "psfs_mc_release", "psfs_roi_pixels"]
 MC_HANDLE_BYTES = 64
 SAMPLE_NEAREST = 0
 SAMPLE_BILINEAR = 1
@@ -133,6 +133,7 @@ def lib():
         L.psfs_mc_attach.argtypes = [vp, vp]
         L.psfs_mc_bind.argtypes = [vp, C.POINTER(vp)]
         L.psfs_mc_release.argtypes = [vp]
+        L.psfs_roi_pixels.argtypes = [vp, C.POINTER(C.c_int64)]
         _lib = L
     return _lib
 
@@ -333,8 +334,10 @@ class Reconstructor:
         4 warp-row loads (see include/psfs.h)."""
         self._check(lib().psfs_set_stage1_path(self._h, int(path)), "psfs_set_stage1_path")
 
-    def set_roi_enabled(self, on: bool):
-        self._check(lib().psfs_set_roi_enabled(self._h, int(bool(on))), "psfs_set_roi_enabled")
+    def set_roi_enabled(self, on):
+        """True: rectangles + per-row spans (default); False: whole images;
+        2: rectangles only (A/B)."""
+        self._check(lib().psfs_set_roi_enabled(self._h, 2 if on == 2 else int(bool(on))), "psfs_set_roi_enabled")
 
     # -- outputs -------------------------------------------------------------
     @property
@@ -594,6 +597,12 @@ class Reconstructor:
         out = np.empty((self.ncam, 12), np.float32)
         self._check(lib().psfs_debug_matrices(self._h, out.ctypes.data), "psfs_debug_matrices")
         return out
+
+    def roi_pixels(self) -> int:
+        """Stage-1 pixels of one frame set (per-row spans, or rectangles)."""
+        v = C.c_int64()
+        self._check(lib().psfs_roi_pixels(self._h, C.byref(v)), "psfs_roi_pixels")
+        return int(v.value)
 
     def roi(self):
         out = np.empty((self.ncam, 4), np.int32)

@@ -402,3 +402,39 @@ def test_c5_coarse_pass_64_frames_sampled():
         mism = bits != (post > 0.5)
         assert not (mism & ~(np.abs(post - 0.5) < 1e-4)).any()
         assert bits.sum() > 0
+
+
+@pytest.mark.parametrize("world", [1, 4])
+def test_row_spans_identical_to_rectangles(world):
+    """Per-row spans of the ROI (stage 1 only computes, and the host path only
+    uploads, the columns each row's projected slab hull covers): the exact and
+    the coarse outputs equal the rectangles' and the whole images', the device
+    and host paths alike, while fewer pixels are processed."""
+    from paper_1311_6811_b200 import from_scene
+    s = make_scene("C2")
+    frames = np.stack([make_frames(s, f % 8) for f in range(20)])
+    fr = torch.from_numpy(frames).cuda()
+    outs = {}
+    for mode in (True, 2, False):
+        for r in range(world):
+            rec = from_scene(s, rank=r, world=world)
+            rec.set_roi_enabled(mode)
+            L, B = rec.alloc_outputs(20)
+            rec.reconstruct_batch(fr, 20, logodds=L, bits=B)          # exact path
+            _, Bc = rec.alloc_outputs(20, logodds=False)
+            rec.reconstruct_batch(fr, 20, bits=Bc)                    # coarse pass
+            hf = torch.from_numpy(frames).pin_memory()
+            Bh = torch.zeros((20, s.grid.nwords), dtype=torch.int32).pin_memory()
+            rec.reconstruct_host(hf, 20, None, Bh)                    # zero-copy upload of the spans
+            torch.cuda.synchronize()
+            outs[(mode, r)] = (L.cpu().numpy(), B.cpu().numpy(), Bc.cpu().numpy(), Bh.numpy().copy(),
+                               rec.roi_pixels())
+    for r in range(world):
+        a, b, c = outs[(True, r)], outs[(2, r)], outs[(False, r)]
+        for k in range(4):
+            assert np.array_equal(a[k], b[k]) and np.array_equal(a[k], c[k]), (r, k)
+        assert np.array_equal(a[1], a[2]) and np.array_equal(a[1], a[3])
+        assert a[4] < b[4] < c[4]
+    orc = oracle.scene_reconstruct(s, frames[0], nthreads=NTHREADS)
+    if world == 1:
+        assert_parity(outs[(True, 0)][0][0], outs[(True, 0)][1][0], orc, s.grid.nvox)
