@@ -483,7 +483,8 @@ int psfs_probe_l1_bandwidth(double *bytes_per_s);
  * blocks_per_sm x 256 threads per SM (1..8): sectors_per_line = 2 is
  * k_voxel16's (lane pairs read the two 32-byte sectors of one line, 3 blocks
  * per SM), 1 is k_voxel_c8's (each lane one 32-byte sector of its own line, 2
- * blocks per SM) -- the measured peaks of their rooflines.
+ * blocks per SM) -- the measured peaks of their rooflines;
+ * 4: lane quads read the four sectors of one line (a 128-byte record's pattern).
  * Errors: PSFS_EINVAL, PSFS_ENOMEM, PSFS_ECUDA. */
 int psfs_probe_gather_bandwidth(int64_t table_bytes, int32_t sectors_per_line, int32_t blocks_per_sm,
                                 double *bytes_per_s);
