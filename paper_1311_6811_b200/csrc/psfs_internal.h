@@ -304,6 +304,13 @@ cudaError_t launch_box_sums(const BoxSumsParams &p, cudaStream_t s);
 cudaError_t launch_mc_fill(uint32_t *mc, int64_t fstride, int64_t w0, int64_t w1, int nf, uint32_t value,
                            cudaStream_t s);
 int voxel_tiles(int xlen, int ylen, int k0, int k1, int ty, int kz);
+// coarse stage-2 tiles: 32 x rows x kz, rows = coarse_tile_rows(rec) (the wide
+// kernel's warps per block for 64-byte records, 8 otherwise)
+#ifndef PSFS_EXP_C8W_NW
+#define PSFS_EXP_C8W_NW 8  // warps per k_voxel_c8w block (4 or 8)
+#endif
+int coarse_tile_rows(int rec);
+int coarse_voxel_tiles(int xlen, int ylen, int k0, int k1, int kz, int rec);
 cudaError_t launch_surface(const uint32_t *bits, uint32_t *surf, int64_t *idx, int64_t capacity,
                            int64_t *count, long long *block_scratch, int xlen, int ylen, int zlen,
                            int k0, int k1, cudaStream_t s, int *launches);
