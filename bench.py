@@ -757,6 +757,16 @@ def run_ours(args):
         kv = per_kernel["k_voxel"]
         kv["all_hit_l1_line_bound"] = {"peak": kv["peak"], "frac": kv["achieved"] / kv["peak"],
                                        "peak_source": kv["peak_source"]}
+        # the L1TEX data pipe returns one wavefront per lane pair's 64-byte record
+        # (per lane's 32-byte record, narrow) whatever the locality: ncu counts 16
+        # per warp request (profiles/r02n_ncu_full.md), i.e. one per voxel-camera
+        # -- the pipe's 1 wavefront/clk/SM sets a floor under the kernel's time
+        wf_launch = nvox * ncam
+        floor_us = wf_launch / (nsm * sm_clk * 1e6) * 1e6
+        kv["l1_data_pipe_bound"] = {
+            "wavefronts_per_launch": wf_launch, "floor_us": floor_us, "frac": floor_us / (v_avg_s * 1e6),
+            "source": "one L1TEX data-pipe wavefront per voxel-camera record (ncu: 16 per warp request, "
+                      "l1tex__data_pipe_lsu_wavefronts) at 1/clk/SM x the run's SM clock; DESIGN.md section 8"}
         kv.update({"bound": "l2_gather", "peak": gather_peak,
                    "fixups_per_step": fixups / max(args.steps, 1),
                    "probe_gbs_by_blocks_per_sm": gather_probe,
