@@ -1064,6 +1064,11 @@ def run_ours(args):
                                  note="300-frame walking / arm-waving sequence in one call (16 distinct "
                                       "frame sets of the sequence, every 19th frame, cycled)")),
         ]
+        legs.append(("C2_overlap128", dict(config="C2", nframes=128, pool=64,
+                                           note="128 frames per call: two 64-frame coarse passes, stage 1 of "
+                                                "the second beside stage 2 of the first (the handle's "
+                                                "overlapped schedule); per-kernel times overlap, so the "
+                                                "headline keeps the one-pass step")))
         if not args.no_c5:
             legs.append(("C5", dict(config="C5", nframes=64, pool=1,
                                     note="one 64-frame coarse pass (1 distinct frame set repeated: host "
