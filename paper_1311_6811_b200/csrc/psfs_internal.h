@@ -136,6 +136,8 @@ struct S1CParams {
     float zoff;          // (-ln p_O - eps) s + bias
     const int32_t *span_info, *span_pre, *span_chunk;  // per-row spans (as S1Params), nullable
     int32_t span_rows;
+    int64_t fstride;     // > 0: frames[f * ncam + c] == frames[c] + f * fstride for every f, c (address arithmetic
+                         // instead of a pointer-table load per frame); 0: use the table
 };
 
 struct VCCam {
