@@ -61,6 +61,7 @@ struct S1Params {
     // group 256 k; when set, n4 counts the spans' groups
     const int32_t *span_info, *span_pre, *span_chunk;
     int32_t span_rows;
+    int64_t fstride;  // > 0: frames[f][c] == frames[0][c] + f * fstride for every f, c (path 6 addresses by arithmetic)
 };
 
 // Stage 2 (voxel) launch description.
