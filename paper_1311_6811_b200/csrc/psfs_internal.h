@@ -307,6 +307,14 @@ cudaError_t launch_box_sums(const BoxSumsParams &p, cudaStream_t s);
 cudaError_t launch_mc_fill(uint32_t *mc, int64_t fstride, int64_t w0, int64_t w1, int nf, uint32_t value,
                            cudaStream_t s);
 int voxel_tiles(int xlen, int ylen, int k0, int k1, int ty, int kz);
+#ifndef PSFS_EXP_BOXZ
+#define PSFS_EXP_BOXZ 0  // 1: k_box_sums_z (z-streaming planes) instead of the in-memory halo box
+#endif
+#ifndef PSFS_EXP_BOXSZ
+// output slices per k_box_sums block (in-memory halo box (32+2) x (8+2) x (BOXSZ+2) in 48 KB: <= 16;
+// k_box_sums_z: any depth)
+#define PSFS_EXP_BOXSZ 8
+#endif
 // coarse stage-2 tiles: 32 x rows x kz, rows = coarse_tile_rows(rec) (the wide
 // kernel's warps per block for 64-byte records, 8 otherwise)
 #ifndef PSFS_EXP_C8W_NW
