@@ -311,8 +311,8 @@ int voxel_tiles(int xlen, int ylen, int k0, int k1, int ty, int kz);
 #define PSFS_EXP_BOXZ 0  // 1: k_box_sums_z (z-streaming planes) instead of the in-memory halo box
 #endif
 #ifndef PSFS_EXP_BOXSZ
-// output slices per k_box_sums block (in-memory halo box (32+2) x (8+2) x (BOXSZ+2) in 48 KB: <= 16;
-// k_box_sums_z: any depth)
+// output slices per k_box_sums block (in-memory halo box (32+2) x (8+2) x (BOXSZ+2): <= 10, one thread
+// per right-edge element; k_box_sums_z: any depth)
 #define PSFS_EXP_BOXSZ 8
 #endif
 // coarse stage-2 tiles: 32 x rows x kz, rows = coarse_tile_rows(rec) (the wide
