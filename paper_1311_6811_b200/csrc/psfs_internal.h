@@ -164,6 +164,9 @@ struct VCParams {
     unsigned long long *tile_counter;
     long long tile_base;
     int32_t ntiles, kz;
+    // k_voxel_c8w: tiles [0, nbig) are kz deep over slices [k0, kzb); the rest are
+    // one slice deep over [kzb, k1) (a finer tail for the persistent grid's last wave)
+    int32_t nbig, kzb;
     uint32_t *bits_base;      // frame f at bits_base + f * bits_stride (nullable when npeer > 0)
     int64_t bits_stride;
     int32_t npeer;
