@@ -1115,9 +1115,10 @@ def run_ours(args):
             "dtype": ("f32+u8+i32 (coarse codes; f64 exact fix-up)" if coarse else "f64+f32+i32"),
             "data": "synthetic",
             "voxel_camera_projections_per_s": fps * nvox * ncam,
-            "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']} -- each frame set "
-                                   f"reconstructed independently, {B} distinct frame sets per step "
-                                   f"({(B + F - 1) // F} pass(es) of {F} frames)",
+            "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}",
+                       "batching": (f"each frame set (one frame of every camera) reconstructed independently; "
+                                    f"{B} distinct frame sets per step per GPU, {(B + F - 1) // F} pass(es) of "
+                                    f"{F} frames"),
                        "frames_per_step_per_gpu": B, "fused_frames_per_pass": F,
                        "path": ("coarse passes (8-bit bracketing codes, exact fix-up; bitmask "
                                 "identical to the exact path)" if coarse else "exact int32 terms"),
