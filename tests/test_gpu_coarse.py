@@ -270,3 +270,25 @@ def test_full_size_wide_pass_vs_oracle(name, nf):
     Bb = _bits(b, fr[:2].contiguous(), 2)
     assert torch.equal(Ba[:2], Bb)
     assert 0 < nfix < 1e-3 * nf * s.grid.nvox
+
+
+# ------------------------------------------------------------------ frame addressing
+
+@pytest.mark.parametrize("coarse_mode", [1, 0])
+def test_strided_and_table_frame_pointers_agree(coarse_mode):
+    """Stage 1 computes per-frame image addresses by arithmetic when the call's
+    frame pointers are uniformly strided (one [frame][camera] tensor), and loads
+    them from the pointer table otherwise (separately allocated images).  Both
+    must give the same bitmask -- coarse passes (k_likelihood_c8p) and the exact
+    path (k_likelihood_x4p) -- and the oracle's bits."""
+    s = make_scene("C1")
+    nf = 24
+    frames = np.stack([make_frames(s, f % 7) for f in range(nf)])
+    strided = torch.from_numpy(frames).cuda()
+    table = [[torch.from_numpy(frames[f, c].copy()).cuda() for c in range(s.ncam)] for f in range(nf)]
+    rec = _rec(s, mode=coarse_mode)
+    Ba = _bits(rec, strided, nf)
+    Bb = _bits(rec, table, nf)
+    assert torch.equal(Ba, Bb)
+    o = oracle.scene_reconstruct(s, frames[5], nthreads=NTHREADS)
+    assert_parity(None, Ba[5].cpu().numpy().view(np.uint32), o, s.grid.nvox)
